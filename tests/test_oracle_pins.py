@@ -1,0 +1,429 @@
+"""Pins of the C oracle against things other than itself (CPU only).
+
+Each test names what fixes the expected value: Random123/curand Philox KATs,
+the paper's worked examples (PAPER.md P:<line>), closed forms, an independent
+numpy density-matrix / matrix-chain simulator (oracle/dms.py), invariants and
+brute force on tiny inputs.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+from oracle import dms
+from workloads import circuits as W
+
+PI, PX, PY, PZ = 0, 1, 2, 3
+
+
+# ------------------------------------------------------------------ Philox (reading #9)
+def test_philox_known_answers(oracle):
+    # Random123 philox4x32-10 known-answer vectors (kat_vectors), the generator curand implements.
+    assert oracle.philox([0, 0, 0, 0], [0, 0]) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    assert oracle.philox([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2) == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    assert oracle.philox([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0]) == \
+        [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+
+
+# ------------------------------------------------------------------ channels / sites
+def test_depolarizing_thresholds(oracle):
+    # p = 0.1 -> I 90 %, X/Y/Z 10/3 % each
+    n, ops = 1, [W.op(W.X, 0)]
+    st = oracle.site_table(n, ops, 0.1, 0.0, 0.0)
+    assert len(st) == 1
+    s = st[0]
+    assert int(s["tX"]) == int(s["tY"]) == int(s["tZ"]) == round(2 ** 32 / 30)
+    assert int(s["tI"]) + 3 * int(s["tX"]) == 2 ** 32
+    assert abs(int(s["tI"]) / 2 ** 32 - 0.9) < 1e-9
+    # bit flip (1-p, p, 0, 0), p = 1 -> deterministic flip
+    st = oracle.site_table(1, [], 0, 0, 1.0)
+    assert int(st[0]["tX"]) == 2 ** 32 and int(st[0]["tI"]) == 0
+
+
+def test_site_counts(oracle):
+    # one site per (gate, acted qubit) (reading #1), measurement sites only when p_meas > 0
+    for name, m in [("C1", 54), ("C2a", 47), ("C3", 569), ("C4", 723)]:
+        cfg = W.config(name)
+        assert len(oracle.site_table(cfg.n, cfg.ops, cfg.noise.p1, cfg.noise.p2, cfg.noise.p_meas)) == m
+    # GHZ(2) with measurement -> 1 + 2 + 2 sites
+    n, ops = W.ghz(2)
+    assert len(oracle.site_table(n, ops, 0.01, 0.01, 0.01)) == 5
+
+
+def test_er_sampler_marginals(oracle):
+    # site marginals converge to (1-p, p/3, p/3, p/3); 4-sigma binomial band
+    n, ops = 1, [W.op(W.H, 0)]
+    p, shots = 0.3, 60000
+    cnt = np.zeros(4)
+    for s in range(shots):
+        er = oracle.sample_er(n, ops, p, 0.0, 0.0, 7, s)
+        cnt[er[0][1] if er else 0] += 1
+    exp = np.array([1 - p, p / 3, p / 3, p / 3]) * shots
+    sig = np.sqrt(exp * (1 - exp / shots))
+    assert np.all(np.abs(cnt - exp) < 4 * sig), (cnt, exp)
+
+
+def test_er_all_identity_frequency(oracle):
+    # all-I frequency ~ (1-p)^M, via the tally of the tree builder
+    n, ops = W.ghz(3)
+    M = 1 + 2 * 2
+    p = 0.05
+    shots = 20000
+    hw0 = sum(1 for s in range(shots) if not oracle.sample_er(n, ops, p, p, 0.0, 3, s))
+    e = (1 - p) ** M * shots
+    assert abs(hw0 - e) < 4 * math.sqrt(e * (1 - e / shots))
+
+
+# ------------------------------------------------------------------ ECM worked examples
+def test_fig_p186_commutation(oracle):
+    # Fig. P:186: on H + CNOT, ER (X after H, II after CX) == (I after H, XX after CX)
+    n, ops = 2, [W.op(W.H, 0), W.op(W.CX, 0, 1)]
+    a = oracle.canonicalize(n, ops, [(0, 0, PX)])
+    b = oracle.canonicalize(n, ops, [(1, 0, PX), (1, 1, PX)])
+    assert a == b == [(2, 0, PX), (2, 1, PX)]
+
+
+def test_fig_p193_rz_blocks_x(oracle):
+    # Fig. P:193: a noisy X is not pushed through RZ(theta)
+    n, ops = 1, [W.op(W.X, 0), W.op(W.RZ, 0, 0, 0.7)]
+    assert oracle.canonicalize(n, ops, [(0, 0, PX)]) == [(1, 0, PX)]
+    # ... but Z passes through RZ (rule 3) and is dropped before measurement (reading #7)
+    assert oracle.canonicalize(n, ops, [(0, 0, PZ)]) == []
+
+
+def test_rule6_y_on_target(oracle):
+    # P:219 rule 6: Y on the CNOT target -> Z on control, Y on target.  Pin it through
+    # blocking gates: H turns Z_c into X_c, then T blocks X_c and Y_t in place.
+    n = 2
+    ops = [W.op(W.I, 1), W.op(W.CX, 0, 1), W.op(W.H, 0), W.op(W.T, 0), W.op(W.T, 1)]
+    assert oracle.canonicalize(n, ops, [(0, 1, PY)]) == [(3, 0, PX), (4, 1, PY)]
+    # rule 4: X on the control -> X on both (both blocked by T)
+    ops = [W.op(W.I, 0), W.op(W.CX, 0, 1), W.op(W.T, 0), W.op(W.T, 1)]
+    assert oracle.canonicalize(n, ops, [(0, 0, PX)]) == [(2, 0, PX), (3, 1, PX)]
+    # rule 1: two noisy X back to back cancel
+    assert oracle.canonicalize(n, ops, [(0, 0, PX), (1, 0, PX), (1, 1, PX)]) == []
+
+
+def test_commutation_soundness_random(oracle):
+    # canonical placement == original placement in |amp|^2, checked with
+    # the independent numpy matrix-chain simulator.
+    rng = np.random.default_rng(11)
+    for trial in range(300):
+        n = int(rng.integers(1, 5))
+        ops = W.random_circuit(rng, n, int(rng.integers(1, 24)))
+        if not ops:
+            continue
+        L = len(ops)
+        ins = []
+        for pos in range(L + 1):
+            qs = range(n) if pos == L else ([ops[pos][1], ops[pos][2]] if ops[pos][0] in W.TWO_QUBIT else [ops[pos][1]])
+            for q in qs:
+                if rng.random() < 0.35:
+                    ins.append((pos, q, int(rng.integers(1, 4))))
+        can = oracle.canonicalize(n, ops, ins)
+        a = np.abs(dms.statevector(n, ops, insert_after=ins)) ** 2
+        b = np.abs(dms.statevector(n, ops, insert_before=can)) ** 2
+        assert np.abs(a - b).max() < 1e-12, (trial, ops, ins, can)
+
+
+def test_monotonicity_S1_S2_S3(oracle):
+    # Fig. P:40: S1 >= S2 >= S3 and shots conserved
+    for name in ["C1", "C2a", "C3"]:
+        cfg = W.config(name)
+        t = oracle.Tree.from_config(cfg)
+        st = t.stats()
+        assert st["S1"] >= st["S2"] >= st["S3"] >= st["n_leaves"] > 0
+        assert sum(t.leaf(l)[1] for l in range(st["n_leaves"])) == cfg.shots
+
+
+def test_ghz_errors_reach_terminal_frame(oracle):
+    # GHZ is H + CNOTs: every noisy Pauli either passes every gate or is dropped
+    # (Z before readout) -- canonical leaves carry only terminal X.
+    cfg = W.config("C2a")
+    t = oracle.Tree.from_config(cfg, prune=False)
+    for l in range(t.n_leaves):
+        tr, _, _ = t.leaf(l)
+        assert all(pos == len(cfg.ops) and p == PX for (pos, q, p) in tr)
+
+
+# ------------------------------------------------------------------ pruning
+def test_pruning_worked_example(oracle):
+    # counts {800,100,50,42,5,3}, alpha = 0.01 -> threshold 8; 5 and 3 insignificant
+    counts = [800, 100, 50, 42, 5, 3]
+    oc, cl, st = oracle.prune(counts, 1, 100, beta=100)
+    assert st["p0"] == 800 and st["n_sig"] == 4 and st["n_insig"] == 2
+    assert list(cl) == [1, 1, 1, 1, 2, 2]
+    assert list(oc) == counts      # |I| <= beta: gamma = 1, exact no-op
+    # beta = 1: one of the two is kept and carries p_insig = 8 shots (P:340 scaling)
+    oc, cl, st = oracle.prune(counts, 1, 100, beta=1)
+    assert st["n_selected"] == 1 and sorted(cl[4:]) == [0, 2]
+    assert oc[4:].sum() == 8 and oc.sum() == sum(counts)
+    # P:415 bound with K = {5}: gamma = 8/5, p0 alpha (|I| + gamma |K|) / S = 0.0288
+    gamma = 8 / 5
+    assert abs(800 * 0.01 * (2 + gamma * 1) / 1000 - 0.0288) < 1e-15
+
+
+def test_pruning_scaling_conserves_shots(oracle):
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        counts = list(rng.integers(1, 40, size=int(rng.integers(1, 400))))
+        counts[int(rng.integers(len(counts)))] = 3000
+        oc, cl, st = oracle.prune(counts, 1, 100, beta=int(rng.integers(1, 120)), seed=int(rng.integers(1 << 30)))
+        assert oc.sum() == sum(counts)
+        for c, o, k in zip(counts, oc, cl):
+            if k == 1:
+                assert o == c and c * 100 >= 3000
+            if k == 2:
+                assert c * 100 < 3000 and o >= c
+
+
+def _exact_mixture(oracle, t, n):
+    P = np.zeros(1 << n)
+    S = 0
+    for l in range(t.n_leaves):
+        tr, c, _ = t.leaf(l)
+        P += c * np.abs(t.replay_leaf(l)) ** 2
+        S += c
+    return P / S
+
+
+def test_pruning_bound_holds(oracle):
+    # max_k |P(k) - P'(k)| <= p0 alpha (|I| + gamma |K|), counts normalized by S
+    rng = np.random.default_rng(8)
+    checked = 0
+    for trial in range(12):
+        n = 4
+        ops = W.random_circuit(rng, n, 14)
+        shots, seed = 3000, int(rng.integers(1, 1 << 30))
+        full = oracle.Tree(n, ops, 0.08, 0.12, 0.05, shots, seed, beta=5, prune=False)
+        pr = oracle.Tree(n, ops, 0.08, 0.12, 0.05, shots, seed, beta=5, prune=True)
+        st = pr.stats()
+        if st["n_insig"] <= 5:
+            continue
+        # gamma = p_insig / sum_K p (original counts of the kept insignificant leaves)
+        full_counts = {tuple(full.leaf(l)[0]): full.leaf(l)[1] for l in range(full.n_leaves)}
+        p0 = st["p0"]
+        insig = [c for c in full_counts.values() if c * 100 < p0]
+        kept = [full_counts[tuple(pr.leaf(l)[0])] for l in range(pr.n_leaves) if full_counts[tuple(pr.leaf(l)[0])] * 100 < p0]
+        gamma = sum(insig) / sum(kept)
+        bound = p0 * 0.01 * (len(insig) + gamma * len(kept)) / shots
+        d = np.abs(_exact_mixture(oracle, full, n) - _exact_mixture(oracle, pr, n)).max()
+        assert d <= bound + 1e-12, (d, bound)
+        checked += 1
+    assert checked >= 3
+
+
+# ------------------------------------------------------------------ DFS order (reading #12)
+def _slot_vector(tr, slots):
+    d = {(p, q): P for (p, q, P) in tr}
+    return tuple(d.get(s, 0) for s in slots)
+
+
+def test_dfs_order_matches_trie_preorder(oracle):
+    # DFS of the trie over slots (pos, q), children I < X < Y < Z, equals lexicographic
+    # order of the per-slot Pauli vectors (brute force over the explicit slot list).
+    cfg = W.config("C1")
+    t = oracle.Tree.from_config(cfg)
+    leaves = [t.leaf(l)[0] for l in range(t.n_leaves)]
+    slots = sorted({(p, q) for tr in leaves for (p, q, _) in tr})
+    vecs = [_slot_vector(tr, slots) for tr in leaves]
+    assert vecs == sorted(vecs)
+    assert len(set(vecs)) == len(vecs)
+    # offsets are the exclusive prefix sum of counts
+    offs = [t.leaf(l)[2] for l in range(t.n_leaves)]
+    cnts = [t.leaf(l)[1] for l in range(t.n_leaves)]
+    assert offs == list(np.concatenate([[0], np.cumsum(cnts)[:-1]]))
+
+
+# ------------------------------------------------------------------ gate application (Eq. 1)
+def test_gates_match_dense_matrix_chain(oracle):
+    # per-gate loops == dense matrix-chain product, n <= 4
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        n = int(rng.integers(1, 5))
+        ops = W.random_circuit(rng, n, int(rng.integers(1, 20)))
+        a = oracle.replay(n, ops, [])
+        b = dms.statevector(n, ops)
+        assert np.abs(a - b).max() < 1e-13
+
+
+def test_gate_examples(oracle):
+    # RZ(pi/2) = diag(e^{-i pi/4}, e^{i pi/4})
+    for b, ph in [(0, -1), (1, 1)]:
+        st = np.zeros(2, dtype=complex)
+        st[b] = 1
+        oracle.apply_gate(st, 1, W.op(W.RZ, 0, 0, math.pi / 2))
+        assert abs(st[b] - np.exp(1j * ph * math.pi / 4)) < 1e-15
+    # CNOT(0,1) (|00> + |01>)/sqrt2 -> (|00> + |11>)/sqrt2
+    st = np.array([1, 1, 0, 0], dtype=complex) / math.sqrt(2)
+    oracle.apply_gate(st, 2, W.op(W.CX, 0, 1))
+    assert np.allclose(st, np.array([1, 0, 0, 1]) / math.sqrt(2), atol=1e-16)
+    # X on qubit 0 of |00> -> |01> (index 1)
+    st = np.array([1, 0, 0, 0], dtype=complex)
+    oracle.apply_gate(st, 2, W.op(W.X, 0))
+    assert st[1] == 1
+
+
+def test_round_trip_inverse(oracle):
+    # G then G^-1 restores the state up to rounding
+    rng = np.random.default_rng(4)
+    n = 5
+    for _ in range(50):
+        ops = W.random_circuit(rng, n, 30)
+        st = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+        st /= np.linalg.norm(st)
+        ref = st.copy()
+        for g in ops:
+            oracle.apply_gate(st, n, g)
+        for g in reversed(ops):
+            oracle.apply_gate(st, n, g, inverse=True)
+        assert np.abs(st - ref).max() < 1e-13
+    # X, CX, Z, Y, S round trips are bit-exact (pure moves, sign and re/im swaps)
+    ops = [W.op(k, 0) for k in (W.X, W.Y, W.Z, W.S)] + [W.op(W.CX, 1, 2)]
+    st = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    ref = st.copy()
+    for g in ops:
+        oracle.apply_gate(st, n, g)
+    for g in reversed(ops):
+        oracle.apply_gate(st, n, g, inverse=True)
+    assert np.array_equal(st, ref)
+
+
+# ------------------------------------------------------------------ closed forms
+def test_ghz_closed_form(oracle):
+    for n in (2, 5, 12):
+        st = oracle.replay(*W.ghz(n), [])
+        ref = np.zeros(1 << n, dtype=complex)
+        ref[0] = ref[-1] = 1 / math.sqrt(2)
+        assert np.abs(st - ref).max() < 1e-15
+
+
+def test_adder_closed_form(oracle):
+    # Noiseless Cuccaro adder is a classical permutation: output |a, a+b> with amplitude 1.
+    for k in (1, 2, 3, 4, 6):
+        n, ops = W.adder(k)
+        st = oracle.replay(n, ops, [])
+        idx = W.adder_expected_output(k)
+        assert abs(st[idx] - 1) < 1e-13
+        assert abs(np.linalg.norm(st) - 1) < 1e-13
+    assert W.adder_expected_output(1) == 0xC
+    assert W.adder_expected_output(11) == 0xE66664
+    assert W.adder_expected_output(14) == 0x26666664
+    # exhaustive operand pairs at k <= 3: replace the X-load prefix
+    for k in (1, 2, 3):
+        n, ops = W.adder(k)
+        a0, b0 = W.adder_operands(k)
+        body = ops[bin(a0).count("1") + bin(b0).count("1"):]
+        for a in range(1 << k):
+            for b in range(1 << k):
+                load = []
+                for i in range(k):
+                    if (a >> i) & 1:
+                        load.append(W.op(W.X, 2 * i + 2))
+                    if (b >> i) & 1:
+                        load.append(W.op(W.X, 2 * i + 1))
+                st = oracle.replay(n, load + body, [])
+                s = a + b
+                idx = sum(((a >> i) & 1) << (2 * i + 2) | ((s >> i) & 1) << (2 * i + 1) for i in range(k))
+                idx |= ((s >> k) & 1) << (2 * k + 1)
+                assert abs(st[idx] - 1) < 1e-13
+
+
+def test_qft_closed_form(oracle):
+    # amplitude(y) = e^{2 pi i x rev_n(y) / 2^n} / sqrt(2^n) (reading #14)
+    for native in (False, True):
+        for n in (3, 6, 9):
+            _, ops = W.qft(n, native)
+            st = oracle.replay(n, ops, [])
+            x = W.qft_input(n)
+            y = np.arange(1 << n)
+            rev = np.array([int(format(v, f"0{n}b")[::-1], 2) for v in y])
+            ref = np.exp(2j * np.pi * ((x * rev) % (1 << n)) / (1 << n)) / math.sqrt(1 << n)
+            assert np.abs(st - ref).max() < 1e-13
+
+
+# ------------------------------------------------------------------ DMS equivalence
+def _enumerate_exact(oracle, n, ops, p1, p2, pm, canonical):
+    sites = oracle.site_table(n, ops, p1, p2, pm)
+    choices = []
+    for s in sites:
+        if int(s["pos"]) == len(ops):
+            choices.append([(PI, 1 - pm), (PX, pm)])
+        else:
+            p = p2 if ops[int(s["pos"])][0] in W.TWO_QUBIT else p1
+            choices.append([(PI, 1 - p), (PX, p / 3), (PY, p / 3), (PZ, p / 3)])
+    P = np.zeros(1 << n)
+    for combo in itertools.product(*choices):
+        w = np.prod([c[1] for c in combo])
+        ins = [(int(s["pos"]), int(s["q"]), c[0]) for s, c in zip(sites, combo) if c[0] != PI]
+        if canonical:
+            st = oracle.replay(n, ops, oracle.canonicalize(n, ops, ins), before_gate=True)
+        else:
+            st = oracle.replay(n, ops, ins, before_gate=False)
+        P += w * np.abs(st) ** 2
+    return P
+
+
+def test_brute_force_matches_dms(oracle):
+    # sum over all ERs of Pr(ER) |psi_ER|^2 == diag(rho) of the DMS.
+    n = 2
+    ops = [W.op(W.H, 0), W.op(W.T, 0), W.op(W.H, 0), W.op(W.CX, 0, 1), W.op(W.T, 1), W.op(W.H, 1)]
+    p1, p2, pm = 0.05, 0.1, 0.07
+    ref = dms.dms_run(n, ops, p1, p2, pm)
+    assert np.abs(ref - [0.35712378, 0.14287622, 0.35712378, 0.14287622]).max() < 1e-8
+    for canonical in (False, True):
+        P = _enumerate_exact(oracle, n, ops, p1, p2, pm, canonical)
+        assert np.abs(P - ref).max() < 1e-12
+
+
+def test_noisy_ghz2_closed_form():
+    # GHZ-2 under p2 on both CX qubits and p_meas: f = 2 p2 / 3, f <- f(1-pm) + (1-f) pm,
+    # P(01) = P(10) = f (1-f) (independent of p1).
+    p1, p2, pm = 1e-3, 1e-2, 0.0
+    n, ops = W.ghz(2)
+    P = dms.dms_run(n, ops, p1, p2, pm)
+    f = 2 * p2 / 3
+    assert abs(P[1] - f * (1 - f)) < 1e-15 and abs(P[1] - 0.00662222) < 1e-8
+    pm = 0.02
+    P = dms.dms_run(n, ops, p1, p2, pm)
+    f = f * (1 - pm) + (1 - f) * pm
+    assert abs(P[2] - f * (1 - f)) < 1e-15
+
+
+@pytest.mark.parametrize("family", ["adder", "ghz", "qft"])
+def test_pipeline_tvd_to_dms(oracle, family):
+    # P:112 (trajectory average -> DMS as S grows): seed-fixed tally + commutation + DFS
+    # pipeline vs DMS, TVD <= 0.01.  Pruning is off here: with beta = 100 its
+    # resampling error (~p_insig/sqrt(beta), reading #10) exceeds 0.01 at p = 1 %;
+    # pruning is pinned by its own bound in test_pruning_bound_holds.
+    if family == "adder":
+        n, ops = W.adder(1)
+    elif family == "ghz":
+        n, ops = W.ghz(4)
+    else:
+        n, ops = W.qft(4)
+    p1, p2, pm = 0.01, 0.01, 0.01
+    ref = dms.dms_run(n, ops, p1, p2, pm)
+    t = oracle.Tree(n, ops, p1, p2, pm, 200000, 2024, prune=False)
+    slots, edge = t.run()
+    hist = np.bincount(slots.astype(np.int64), minlength=1 << n) / len(slots)
+    assert 0.5 * np.abs(hist - ref).sum() <= 0.01
+
+
+# ------------------------------------------------------------------ sampling
+def test_sampling_examples(oracle):
+    # |01> -> every draw is index 1
+    st = np.zeros(4, dtype=complex)
+    st[1] = 1
+    out, edge = oracle.sample_state(st, 2, 1, 0, 100)
+    assert np.all(out == 1) and not edge.any()
+    # (|0> + |1>)/sqrt2, 10^5 draws within 4 sigma of 1/2
+    st = np.array([1, 1], dtype=complex) / math.sqrt(2)
+    out, _ = oracle.sample_state(st, 1, 9, 3, 100000)
+    assert abs(int(out.sum()) - 50000) < 4 * math.sqrt(25000)
+    # zero-probability outcomes are never drawn (strict C(k) > t)
+    st = np.array([0, 0.6, 0, 0.8], dtype=complex)
+    out, _ = oracle.sample_state(st, 2, 2, 0, 20000)
+    assert set(np.unique(out)) <= {1, 3}
+    assert abs((out == 3).mean() - 0.64) < 0.02
