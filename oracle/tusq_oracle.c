@@ -488,6 +488,7 @@ int or_build(uint32_t n, const or_op *ops, uint64_t L, double p1, double p2, dou
 {
     *out = NULL;
     if (or_validate(n, ops, L) || shots == 0 || a_den == 0) return 1;
+    if (prune_enabled && (beta == 0 || a_num > a_den)) return 1;   /* beta >= 1 keeps shots conserved */
     if (!(p1 >= 0 && p1 <= 1) || !(p2 >= 0 && p2 <= 1) || !(pm >= 0 && pm <= 1)) return 1;
     uint64_t m = or_site_table(n, ops, L, p1, p2, pm, NULL);
     or_site *sites = (or_site *)malloc((m ? m : 1) * sizeof(or_site));

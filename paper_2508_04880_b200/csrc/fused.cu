@@ -1,0 +1,923 @@
+// K5: fused-tile gate kernel and its host planner.
+//
+// One launch applies a run of gates (a "group") to the whole 2^n state in ONE HBM sweep
+// (read + write 2 * 2^n * s bytes), instead of one sweep per gate (Eq. 1: a k-qubit
+// gate touches only its own amplitude pairs, so gates confined to a 12-qubit tile commute with
+// the tiling).  Design:
+//   - a tile = the 4096 amplitudes that share the values of the n-12 "outer" qubits; tile qubits
+//     are qubits 0,1,2 (128-byte contiguous runs) plus the group's exchange qubits plus fillers;
+//   - 128 threads x 32 register-resident amplitudes; 5 "register" tile bits, 5 lane bits, 2 warp
+//     bits.  A gate that exchanges amplitudes (H, RX, RY, U, X, Y, CX target) needs its qubit in a
+//     register bit: the planner splits the group into phases with different register sets and the
+//     kernel switches phases by one shared-memory transpose (XOR-swizzled, conflict-free when
+//     lanes 0-2 carry qubits 0-2);
+//   - diagonal gates and CX/CZ/CP controls act on ANY qubit: register bits at compile-time
+//     positions, thread/outer bits through per-thread predicates on the logical index;
+//   - H is applied as an unscaled butterfly; the (1/sqrt2)^h factor (and global phases of
+//     relabelled Y) is applied once at the store;
+//   - X (and the X part of Y) on a qubit's first or last touch in a group is a free RELABEL:
+//     the state is stored as physical = logical XOR mask, loads/stores XOR their addresses,
+//     and the tile part of the mask is materialized by the next sweep at no cost;
+//   - a reset to a basis state (K7) is fused into the first sweep (no load);
+//   - the last sweep before sampling can emit per-4096-block |amp|^2 sums (K6 epilogue).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "fused.h"
+#include "kernels.h"
+
+namespace tq {
+namespace fk {
+
+constexpr int TB = 12;     // tile bits
+constexpr int RB = 5;      // register bits
+constexpr int NR = 32;     // amplitudes per thread
+constexpr int NT = 128;    // threads per CTA
+constexpr int MAXPH = 24;
+constexpr int MAXG = 400;
+constexpr int MAXP = 900;
+
+enum Code : uint16_t {
+    C_H = 0,      // +r      unscaled butterfly
+    C_U = 5,      // +r      generic 2x2 (8 params)
+    C_X = 10,     // +r
+    C_Y = 15,     // +r
+    C_D1 = 20,    // +r      bit 1 *= p (2 params)
+    C_D2 = 25,    // +r      bit 0 *= p0, bit 1 *= p1 (4 params)
+    C_CX = 30,    // +5c+t   (c != t)
+    C_CPH = 55,   // +5a+b   (a < b) both bits 1 *= p
+    C_TX = 80,    // +t      if pred(q): X on reg t
+    C_TD1 = 85,   // +r      if pred(q): bit 1 of reg r *= p
+    C_TPH = 90,   //         all *= pred(q0)&pred(q1) ? p1 : p0 (4 params)
+    C_N = 91
+};
+
+struct Phase {
+    uint16_t g0, g1;      // gate range
+    uint8_t rl[RB];       // tile-local bit of each register bit
+    uint8_t tl[7];        // tile-local bit of each thread bit (lanes 0-4, warps 0-1)
+};
+
+struct GRec {
+    uint16_t code;
+    uint8_t a, b;         // TX/TD1: a = global control qubit; TPH: a, b = global qubits
+    uint16_t pi;          // parameter index into prm
+    uint16_t _pad;
+};
+
+enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4 };
+
+struct Params {
+    uint64_t xm_load, xm_store;   // physical = logical ^ mask at load / at store
+    uint64_t init_index;          // F_INIT: virtual memory holds init amp at physical init_index
+    double init_re, init_im;
+    double scale_re, scale_im;
+    uint64_t ntiles;
+    uint32_t flags, nphase;
+    uint8_t qs[TB];               // tile-local bit b <-> global qubit qs[b] (ascending)
+    uint32_t _pad;
+    Phase ph[MAXPH];
+    GRec g[MAXG];
+    double prm[MAXP];
+};
+static_assert(sizeof(Params) < 32000, "kernel parameter block too large");
+
+template <typename R> struct CV;
+template <> struct CV<double> { using T = double2; };
+template <> struct CV<float> { using T = float2; };
+
+__device__ __forceinline__ uint64_t ins0(uint64_t j, uint32_t q)
+{
+    return ((j >> q) << (q + 1)) | (j & ((1ull << q) - 1));
+}
+
+template <typename V, typename R>
+__device__ __forceinline__ V mulc(V a, R pr, R pi)
+{
+    V r;
+    r.x = a.x * pr - a.y * pi;
+    r.y = a.x * pi + a.y * pr;
+    return r;
+}
+
+// ---------------------------------------------------------------- register gate ops
+template <int B, typename V>
+__device__ __forceinline__ void g_h(V (&a)[NR])
+{
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+        if (!(i & (1 << B))) {
+            V x = a[i], y = a[i | (1 << B)];
+            a[i].x = x.x + y.x; a[i].y = x.y + y.y;
+            a[i | (1 << B)].x = x.x - y.x; a[i | (1 << B)].y = x.y - y.y;
+        }
+}
+
+template <int B, typename V, typename R>
+__device__ __forceinline__ void g_u(V (&a)[NR], const double *p)
+{
+    const R u0r = (R)p[0], u0i = (R)p[1], u1r = (R)p[2], u1i = (R)p[3];
+    const R u2r = (R)p[4], u2i = (R)p[5], u3r = (R)p[6], u3i = (R)p[7];
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+        if (!(i & (1 << B))) {
+            V x = a[i], y = a[i | (1 << B)];
+            a[i].x = u0r * x.x - u0i * x.y + u1r * y.x - u1i * y.y;
+            a[i].y = u0r * x.y + u0i * x.x + u1r * y.y + u1i * y.x;
+            a[i | (1 << B)].x = u2r * x.x - u2i * x.y + u3r * y.x - u3i * y.y;
+            a[i | (1 << B)].y = u2r * x.y + u2i * x.x + u3r * y.y + u3i * y.x;
+        }
+}
+
+template <int B, typename V>
+__device__ __forceinline__ void g_x(V (&a)[NR])
+{
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+        if (!(i & (1 << B))) {
+            V x = a[i];
+            a[i] = a[i | (1 << B)];
+            a[i | (1 << B)] = x;
+        }
+}
+
+template <int B, typename V>
+__device__ __forceinline__ void g_y(V (&a)[NR])
+{
+    // (Y psi)_0 = -i psi_1, (Y psi)_1 = i psi_0
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+        if (!(i & (1 << B))) {
+            V x = a[i], y = a[i | (1 << B)];
+            a[i].x = y.y; a[i].y = -y.x;
+            a[i | (1 << B)].x = -x.y; a[i | (1 << B)].y = x.x;
+        }
+}
+
+template <int B, typename V, typename R>
+__device__ __forceinline__ void g_d1(V (&a)[NR], R pr, R pi)
+{
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+        if (i & (1 << B)) a[i] = mulc(a[i], pr, pi);
+}
+
+template <int B, typename V, typename R>
+__device__ __forceinline__ void g_d2(V (&a)[NR], const double *p)
+{
+#pragma unroll
+    for (int i = 0; i < NR; ++i) a[i] = (i & (1 << B)) ? mulc(a[i], (R)p[2], (R)p[3]) : mulc(a[i], (R)p[0], (R)p[1]);
+}
+
+template <int C, int T, typename V>
+__device__ __forceinline__ void g_cx(V (&a)[NR])
+{
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+        if ((i & (1 << C)) && !(i & (1 << T))) {
+            V x = a[i];
+            a[i] = a[i | (1 << T)];
+            a[i | (1 << T)] = x;
+        }
+}
+
+template <int A, int B, typename V, typename R>
+__device__ __forceinline__ void g_cph(V (&a)[NR], R pr, R pi)
+{
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+        if ((i & (1 << A)) && (i & (1 << B))) a[i] = mulc(a[i], pr, pi);
+}
+
+template <typename V, typename R>
+__device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const double *prm, uint64_t lbase)
+{
+    const double *p = prm + g.pi;
+#define TQ_R5(base, fn)                      \
+    case base + 0: fn<0>; break;             \
+    case base + 1: fn<1>; break;             \
+    case base + 2: fn<2>; break;             \
+    case base + 3: fn<3>; break;             \
+    case base + 4: fn<4>; break;
+#define TQ_CX(c, t) case C_CX + 5 * c + t: g_cx<c, t>(a); break;
+#define TQ_CP(x, y) case C_CPH + 5 * x + y: g_cph<x, y, V, R>(a, (R)p[0], (R)p[1]); break;
+    switch (g.code) {
+    case C_H + 0: g_h<0>(a); break;
+    case C_H + 1: g_h<1>(a); break;
+    case C_H + 2: g_h<2>(a); break;
+    case C_H + 3: g_h<3>(a); break;
+    case C_H + 4: g_h<4>(a); break;
+    case C_U + 0: g_u<0, V, R>(a, p); break;
+    case C_U + 1: g_u<1, V, R>(a, p); break;
+    case C_U + 2: g_u<2, V, R>(a, p); break;
+    case C_U + 3: g_u<3, V, R>(a, p); break;
+    case C_U + 4: g_u<4, V, R>(a, p); break;
+    case C_X + 0: g_x<0>(a); break;
+    case C_X + 1: g_x<1>(a); break;
+    case C_X + 2: g_x<2>(a); break;
+    case C_X + 3: g_x<3>(a); break;
+    case C_X + 4: g_x<4>(a); break;
+    case C_Y + 0: g_y<0>(a); break;
+    case C_Y + 1: g_y<1>(a); break;
+    case C_Y + 2: g_y<2>(a); break;
+    case C_Y + 3: g_y<3>(a); break;
+    case C_Y + 4: g_y<4>(a); break;
+    case C_D1 + 0: g_d1<0, V, R>(a, (R)p[0], (R)p[1]); break;
+    case C_D1 + 1: g_d1<1, V, R>(a, (R)p[0], (R)p[1]); break;
+    case C_D1 + 2: g_d1<2, V, R>(a, (R)p[0], (R)p[1]); break;
+    case C_D1 + 3: g_d1<3, V, R>(a, (R)p[0], (R)p[1]); break;
+    case C_D1 + 4: g_d1<4, V, R>(a, (R)p[0], (R)p[1]); break;
+    case C_D2 + 0: g_d2<0, V, R>(a, p); break;
+    case C_D2 + 1: g_d2<1, V, R>(a, p); break;
+    case C_D2 + 2: g_d2<2, V, R>(a, p); break;
+    case C_D2 + 3: g_d2<3, V, R>(a, p); break;
+    case C_D2 + 4: g_d2<4, V, R>(a, p); break;
+    TQ_CX(0, 1) TQ_CX(0, 2) TQ_CX(0, 3) TQ_CX(0, 4)
+    TQ_CX(1, 0) TQ_CX(1, 2) TQ_CX(1, 3) TQ_CX(1, 4)
+    TQ_CX(2, 0) TQ_CX(2, 1) TQ_CX(2, 3) TQ_CX(2, 4)
+    TQ_CX(3, 0) TQ_CX(3, 1) TQ_CX(3, 2) TQ_CX(3, 4)
+    TQ_CX(4, 0) TQ_CX(4, 1) TQ_CX(4, 2) TQ_CX(4, 3)
+    TQ_CP(0, 1) TQ_CP(0, 2) TQ_CP(0, 3) TQ_CP(0, 4)
+    TQ_CP(1, 2) TQ_CP(1, 3) TQ_CP(1, 4)
+    TQ_CP(2, 3) TQ_CP(2, 4)
+    TQ_CP(3, 4)
+    default: {
+        const bool pa = (lbase >> g.a) & 1;
+        if (g.code == C_TPH) {
+            const bool pred = pa && ((lbase >> g.b) & 1);
+            const R fr = (R)(pred ? p[2] : p[0]), fi = (R)(pred ? p[3] : p[1]);
+            if (fr != R(1) || fi != R(0)) {
+#pragma unroll
+                for (int i = 0; i < NR; ++i) a[i] = mulc(a[i], fr, fi);
+            }
+        } else if (pa) {
+            switch (g.code) {
+            case C_TX + 0: g_x<0>(a); break;
+            case C_TX + 1: g_x<1>(a); break;
+            case C_TX + 2: g_x<2>(a); break;
+            case C_TX + 3: g_x<3>(a); break;
+            case C_TX + 4: g_x<4>(a); break;
+            case C_TD1 + 0: g_d1<0, V, R>(a, (R)p[0], (R)p[1]); break;
+            case C_TD1 + 1: g_d1<1, V, R>(a, (R)p[0], (R)p[1]); break;
+            case C_TD1 + 2: g_d1<2, V, R>(a, (R)p[0], (R)p[1]); break;
+            case C_TD1 + 3: g_d1<3, V, R>(a, (R)p[0], (R)p[1]); break;
+            case C_TD1 + 4: g_d1<4, V, R>(a, (R)p[0], (R)p[1]); break;
+            default: break;
+            }
+        }
+    }
+    }
+#undef TQ_R5
+#undef TQ_CX
+#undef TQ_CP
+}
+
+__device__ __forceinline__ uint32_t swz(uint32_t t) { return t ^ ((t >> 3) & 7u); }
+
+template <int R_>
+__device__ __forceinline__ uint32_t roff32(const uint32_t (&rb)[RB])
+{
+    uint32_t o = 0;
+#pragma unroll
+    for (int k = 0; k < RB; ++k)
+        if (R_ & (1 << k)) o |= rb[k];
+    return o;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ psi, const __grid_constant__ Params P,
+                                             double *__restrict__ sums)
+{
+    using V = typename CV<R>::T;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    V *sm = reinterpret_cast<V *>(smraw);
+    __shared__ double red[NT / 32];
+    const uint32_t tid = threadIdx.x;
+    V a[NR];
+    for (uint64_t T = blockIdx.x; T < P.ntiles; T += gridDim.x) {
+        // logical tile base: the tile index deposited into the outer (non-tile) qubit positions
+        uint64_t base = T;
+#pragma unroll
+        for (int b = 0; b < TB; ++b) base = ins0(base, P.qs[b]);
+
+        // ---- phase 0 layout: global offsets of thread bits and register bits
+        uint64_t gthr = 0, greg[RB];
+        {
+            const Phase &p0 = P.ph[0];
+#pragma unroll
+            for (int j = 0; j < 7; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[p0.tl[j]];
+#pragma unroll
+            for (int k = 0; k < RB; ++k) greg[k] = 1ull << P.qs[p0.rl[k]];
+        }
+        if (P.flags & F_INIT) {
+            const uint64_t lt = (base | gthr) ^ P.xm_load;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                uint64_t o = 0;
+#pragma unroll
+                for (int k = 0; k < RB; ++k)
+                    if (r & (1 << k)) o ^= greg[k];
+                const bool hit = (lt ^ o) == P.init_index;
+                a[r].x = hit ? (R)P.init_re : R(0);
+                a[r].y = hit ? (R)P.init_im : R(0);
+            }
+        } else {
+            const uint64_t pld = (base | gthr) ^ P.xm_load;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                uint64_t o = 0;
+#pragma unroll
+                for (int k = 0; k < RB; ++k)
+                    if (r & (1 << k)) o ^= greg[k];
+                a[r] = __ldcs(psi + (pld ^ o));
+            }
+        }
+
+        for (uint32_t ph = 0; ph < P.nphase; ++ph) {
+            const Phase &cur = P.ph[ph];
+            if (ph > 0) {
+                // transpose registers from the previous layout to this one through shared memory
+                const Phase &prv = P.ph[ph - 1];
+                uint32_t tt = 0, rb[RB];
+#pragma unroll
+                for (int j = 0; j < 7; ++j) tt |= ((tid >> j) & 1u) << prv.tl[j];
+#pragma unroll
+                for (int k = 0; k < RB; ++k) rb[k] = 1u << prv.rl[k];
+                __syncthreads();
+#define TQ_ST(r) sm[swz(tt | roff32<r>(rb))] = a[r];
+                TQ_ST(0) TQ_ST(1) TQ_ST(2) TQ_ST(3) TQ_ST(4) TQ_ST(5) TQ_ST(6) TQ_ST(7)
+                TQ_ST(8) TQ_ST(9) TQ_ST(10) TQ_ST(11) TQ_ST(12) TQ_ST(13) TQ_ST(14) TQ_ST(15)
+                TQ_ST(16) TQ_ST(17) TQ_ST(18) TQ_ST(19) TQ_ST(20) TQ_ST(21) TQ_ST(22) TQ_ST(23)
+                TQ_ST(24) TQ_ST(25) TQ_ST(26) TQ_ST(27) TQ_ST(28) TQ_ST(29) TQ_ST(30) TQ_ST(31)
+#undef TQ_ST
+                __syncthreads();
+                tt = 0;
+#pragma unroll
+                for (int j = 0; j < 7; ++j) tt |= ((tid >> j) & 1u) << cur.tl[j];
+#pragma unroll
+                for (int k = 0; k < RB; ++k) rb[k] = 1u << cur.rl[k];
+#define TQ_LD(r) a[r] = sm[swz(tt | roff32<r>(rb))];
+                TQ_LD(0) TQ_LD(1) TQ_LD(2) TQ_LD(3) TQ_LD(4) TQ_LD(5) TQ_LD(6) TQ_LD(7)
+                TQ_LD(8) TQ_LD(9) TQ_LD(10) TQ_LD(11) TQ_LD(12) TQ_LD(13) TQ_LD(14) TQ_LD(15)
+                TQ_LD(16) TQ_LD(17) TQ_LD(18) TQ_LD(19) TQ_LD(20) TQ_LD(21) TQ_LD(22) TQ_LD(23)
+                TQ_LD(24) TQ_LD(25) TQ_LD(26) TQ_LD(27) TQ_LD(28) TQ_LD(29) TQ_LD(30) TQ_LD(31)
+#undef TQ_LD
+            }
+            // logical index bits of this thread (thread + outer bits) for predicates
+            uint64_t lbase = base;
+#pragma unroll
+            for (int j = 0; j < 7; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[cur.tl[j]];
+            for (uint32_t gi = cur.g0; gi < cur.g1; ++gi) apply_gate<V, R>(a, P.g[gi], P.prm, lbase);
+        }
+
+        // ---- store with the last layout
+        const Phase &last = P.ph[P.nphase - 1];
+        gthr = 0;
+#pragma unroll
+        for (int j = 0; j < 7; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[last.tl[j]];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) greg[k] = 1ull << P.qs[last.rl[k]];
+        if (P.flags & F_SCALE) {
+            const R sr = (R)P.scale_re, si = (R)P.scale_im;
+            if (si == R(0)) {
+#pragma unroll
+                for (int r = 0; r < NR; ++r) { a[r].x *= sr; a[r].y *= sr; }
+            } else {
+#pragma unroll
+                for (int r = 0; r < NR; ++r) a[r] = mulc(a[r], sr, si);
+            }
+        }
+        const uint64_t pst = (base | gthr) ^ P.xm_store;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            uint64_t o = 0;
+#pragma unroll
+            for (int k = 0; k < RB; ++k)
+                if (r & (1 << k)) o ^= greg[k];
+            __stcs(psi + (pst ^ o), a[r]);
+        }
+        if (P.flags & F_SUMS) {
+            double s = 0.0;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                double re = a[r].x, im = a[r].y;
+                s += re * re + im * im;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+            if ((tid & 31) == 0) red[tid >> 5] = s;
+            __syncthreads();
+            if (tid == 0) sums[(base ^ P.xm_store) >> TB] = red[0] + red[1] + red[2] + red[3];
+            __syncthreads();
+        }
+    }
+}
+
+}  // namespace fk
+
+// ======================================================================= host planner
+namespace {
+
+using namespace fk;
+
+struct KOp {
+    Op op;
+    bool in_tile_xy = false;   // X/Y applied in registers
+    bool zpart = false;        // Z part of a relabelled Y (diag -1 on q)
+};
+
+struct Group {
+    std::vector<KOp> ops;      // in-kernel ops
+    uint64_t xb = 0, xa = 0;   // relabel masks before load / after store
+    double fr = 1.0, fi = 0.0; // global phase from relabelled Y
+    int nh = 0;                // unscaled H count
+    uint64_t tilemask = 0;     // required tile qubits (exchange operands)
+};
+
+inline uint64_t bit(uint32_t q) { return 1ull << q; }
+
+bool is_exchange(const Op &o) { return o.kind == H || o.kind == RX || o.kind == RY; }
+
+uint64_t op_qubits(const Op &o) { return bit(o.q0) | (two_qubit(o.kind) ? bit(o.q1) : 0); }
+
+}  // namespace
+
+GateTimer::~GateTimer()
+{
+    for (auto e : a_) cudaEventDestroy(e);
+    for (auto e : b_) cudaEventDestroy(e);
+}
+
+void GateTimer::begin(cudaStream_t st)
+{
+    if (!on_) return;
+    if (used_ == a_.size()) {
+        if (a_.size() >= 256) flush();
+        if (used_ == a_.size()) {
+            cudaEvent_t x, y;
+            cudaEventCreate(&x);
+            cudaEventCreate(&y);
+            a_.push_back(x);
+            b_.push_back(y);
+            by_.push_back(0);
+        }
+    }
+    cudaEventRecord(a_[used_], st);
+}
+
+void GateTimer::end(cudaStream_t st, double bytes)
+{
+    if (!on_) return;
+    cudaEventRecord(b_[used_], st);
+    by_[used_] = bytes;
+    ++used_;
+}
+
+void GateTimer::flush()
+{
+    if (!on_ || !used_) return;
+    cudaEventSynchronize(b_[used_ - 1]);
+    for (size_t i = 0; i < used_; ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a_[i], b_[i]);
+        seconds += ms * 1e-3;
+        bytes += by_[i];
+        ++launches;
+    }
+    used_ = 0;
+}
+
+static void count(Ctx &ctx, double bytes, bool fused)
+{
+    ctx.stats->launches++;
+    ctx.stats->sweeps++;
+    ctx.stats->hbm_bytes += bytes;
+    if (fused) ctx.stats->fused_launches++;
+}
+
+void execute_unfused(const std::vector<Op> &ops, Ctx &ctx)
+{
+    size_t i = 0;
+    while (i < ops.size()) {
+        const Op &o = ops[i];
+        if (o.kind == X || o.kind == Y || o.kind == Z) {
+            uint64_t xm = 0, zm = 0, used = 0;
+            size_t j = i;
+            while (j < ops.size() && (ops[j].kind == X || ops[j].kind == Y || ops[j].kind == Z) &&
+                   !((used >> ops[j].q0) & 1)) {
+                used |= bit(ops[j].q0);
+                if (ops[j].kind != Z) xm |= bit(ops[j].q0);
+                if (ops[j].kind != X) zm |= bit(ops[j].q0);
+                ++j;
+            }
+            double b = 0;
+            if (!ctx.dry) {
+                if (ctx.timer) ctx.timer->begin(ctx.st);
+                b = launch_pauli_string(ctx.psi, ctx.n, ctx.prec, xm, zm, ctx.st);
+                if (ctx.timer) ctx.timer->end(ctx.st, b);
+            } else {
+                b = (double)(1ull << ctx.n) * (ctx.prec == 128 ? 16 : 8) * (xm ? 2.0 : 1.0);
+            }
+            count(ctx, b, false);
+            i = j;
+            continue;
+        }
+        if (o.kind != I) {
+            double b;
+            if (!ctx.dry) {
+                if (ctx.timer) ctx.timer->begin(ctx.st);
+                b = launch_gate(ctx.psi, ctx.n, ctx.prec, o, ctx.st);
+                if (ctx.timer) ctx.timer->end(ctx.st, b);
+            } else {
+                double s = (double)(1ull << ctx.n) * (ctx.prec == 128 ? 16 : 8);
+                b = (o.kind == CX || o.kind == T || o.kind == TDG || o.kind == S || o.kind == SDG || o.kind == P)
+                        ? s
+                        : (o.kind == CZ || o.kind == CP) ? 0.5 * s : 2 * s;
+            }
+            count(ctx, b, false);
+        }
+        ++i;
+    }
+}
+
+FusedPlanner::FusedPlanner(uint32_t n, int prec, uint32_t tile_bits)
+    : n_(n), prec_(prec), tile_bits_(TB), enabled_(n >= (uint32_t)TB)
+{
+    (void)tile_bits;
+}
+
+// ---- group formation (greedy over the op stream) --------------------------------------
+static std::vector<Group> make_groups(const std::vector<Op> &ops)
+{
+    const uint64_t low = 7;   // qubits 0,1,2 are always tile qubits
+    std::vector<Group> groups;
+    Group g;
+    uint64_t touched = 0;
+    std::vector<int> pending(64, -1);   // index (in g.ops) of a pending X/Y on qubit q
+    auto popc_hi = [&](uint64_t m) { return __builtin_popcountll(m & ~low); };
+    auto close = [&]() {
+        // pending X/Y become relabel-after (last touch in the group)
+        std::vector<KOp> kept;
+        kept.reserve(g.ops.size());
+        std::vector<uint8_t> drop(g.ops.size(), 0);
+        for (uint32_t q = 0; q < 64; ++q) {
+            int idx = pending[q];
+            if (idx < 0) continue;
+            KOp &k = g.ops[idx];
+            g.xa ^= bit(q);
+            if (k.op.kind == Y) {     // Y = i X Z: Z here, X after the store, factor i
+                k.op.kind = Z;
+                k.zpart = true;
+                double r = g.fr, im = g.fi;
+                g.fr = -im; g.fi = r;
+            } else {
+                drop[idx] = 1;
+            }
+            pending[q] = -1;
+        }
+        for (size_t i = 0; i < g.ops.size(); ++i)
+            if (!drop[i]) kept.push_back(g.ops[i]);
+        g.ops.swap(kept);
+        if (!g.ops.empty() || g.xb || g.xa) groups.push_back(g);
+        g = Group();
+        touched = 0;
+    };
+    for (const Op &o : ops) {
+        if (o.kind == I) continue;
+        const uint64_t qm = op_qubits(o);
+        // requirements of this op on the group's tile set
+        uint64_t need = 0;
+        if (is_exchange(o)) need |= bit(o.q0);
+        if (o.kind == CX) need |= bit(o.q1);
+        // a pending X/Y on a qubit this op touches must be applied in registers
+        for (uint64_t m = qm; m; m &= m - 1) {
+            uint32_t q = __builtin_ctzll(m);
+            if (pending[q] >= 0) need |= bit(q);
+        }
+        const bool xy = (o.kind == X || o.kind == Y);
+        const bool fits = popc_hi(g.tilemask | need) <= TB - 3 && g.ops.size() + 1 < (size_t)MAXG - 8;
+        if (!fits) close();
+        // re-evaluate after a possible close (pending cleared)
+        need = 0;
+        if (is_exchange(o)) need |= bit(o.q0);
+        if (o.kind == CX) need |= bit(o.q1);
+        for (uint64_t m = qm; m; m &= m - 1) {
+            uint32_t q = __builtin_ctzll(m);
+            if (pending[q] >= 0) {
+                need |= bit(q);
+                g.ops[pending[q]].in_tile_xy = true;
+                pending[q] = -1;
+            }
+        }
+        g.tilemask |= need;
+        if (xy) {
+            const uint32_t q = o.q0;
+            if (!(touched & bit(q))) {
+                // first touch: relabel before the load.  Y = (-i) Z X: X first, Z here.
+                g.xb ^= bit(q);
+                if (o.kind == Y) {
+                    KOp k;
+                    k.op = Op{Z, q, 0, 0.0};
+                    k.zpart = true;
+                    g.ops.push_back(k);
+                    double r = g.fr, im = g.fi;   // multiply by -i
+                    g.fr = im; g.fi = -r;
+                }
+            } else {
+                KOp k;
+                k.op = o;
+                g.ops.push_back(k);
+                pending[q] = (int)g.ops.size() - 1;
+            }
+            touched |= bit(q);
+            continue;
+        }
+        KOp k;
+        k.op = o;
+        g.ops.push_back(k);
+        touched |= qm;
+    }
+    close();
+    return groups;
+}
+
+// ---- phase planning + parameter block ----------------------------------------------------
+struct Built {
+    Params P;
+    uint64_t tile = 0;
+};
+
+static void matrix_u(const Op &o, double m[8])
+{
+    const double c = cos(o.theta / 2), s = sin(o.theta / 2);
+    if (o.kind == RX) { double v[8] = {c, 0, 0, -s, 0, -s, c, 0}; memcpy(m, v, sizeof(v)); }
+    else { double v[8] = {c, 0, -s, 0, s, 0, c, 0}; memcpy(m, v, sizeof(v)); }   // RY
+}
+
+static bool diag_of(const Op &o, double d[4])
+{
+    const double s2 = M_SQRT1_2;
+    d[0] = 1; d[1] = 0;
+    switch (o.kind) {
+    case Z: d[2] = -1; d[3] = 0; return true;
+    case S: d[2] = 0; d[3] = 1; return true;
+    case SDG: d[2] = 0; d[3] = -1; return true;
+    case T: d[2] = s2; d[3] = s2; return true;
+    case TDG: d[2] = s2; d[3] = -s2; return true;
+    case P: d[2] = cos(o.theta); d[3] = sin(o.theta); return true;
+    case RZ: d[0] = cos(o.theta / 2); d[1] = -sin(o.theta / 2); d[2] = cos(o.theta / 2); d[3] = sin(o.theta / 2);
+        return true;
+    default: return false;
+    }
+}
+
+static void build_params(const Group &G, uint32_t n, Built &B)
+{
+    Params &P = B.P;
+    memset(&P, 0, sizeof(P));
+    // tile qubits: 0,1,2 + required + fillers (lowest unused)
+    uint64_t tile = G.tilemask | 7ull;
+    for (uint32_t q = 0; __builtin_popcountll(tile) < TB && q < n; ++q) tile |= bit(q);
+    B.tile = tile;
+    uint8_t loc[64];
+    memset(loc, 0xff, sizeof(loc));
+    {
+        int b = 0;
+        for (uint32_t q = 0; q < n; ++q)
+            if (tile & bit(q)) { P.qs[b] = (uint8_t)q; loc[q] = (uint8_t)b; ++b; }
+    }
+    // register-need sequence
+    std::vector<int> needq(G.ops.size(), -1);
+    for (size_t i = 0; i < G.ops.size(); ++i) {
+        const Op &o = G.ops[i].op;
+        if (is_exchange(o) || G.ops[i].in_tile_xy) needq[i] = (int)o.q0;
+        else if (o.kind == CX) needq[i] = (int)o.q1;
+    }
+    auto lookahead = [&](size_t from, uint64_t keep) {
+        std::vector<uint32_t> rs;
+        uint64_t have = 0;
+        for (size_t i = from; i < G.ops.size() && rs.size() < (size_t)RB; ++i)
+            if (needq[i] >= 0 && !(have & bit(needq[i]))) { have |= bit(needq[i]); rs.push_back(needq[i]); }
+        // fill: keep previous register qubits, then tile qubits touched by diagonals, then any >= 3
+        for (uint64_t m = keep; m && rs.size() < (size_t)RB; m &= m - 1) {
+            uint32_t q = __builtin_ctzll(m);
+            if (!(have & bit(q))) { have |= bit(q); rs.push_back(q); }
+        }
+        for (int pass = 0; pass < 2 && rs.size() < (size_t)RB; ++pass)
+            for (uint32_t b = (pass ? 3 : 0); b < (uint32_t)TB && rs.size() < (size_t)RB; ++b) {
+                uint32_t q = P.qs[b];
+                if (pass == 0 && b < 3) continue;
+                if (!(have & bit(q))) { have |= bit(q); rs.push_back(q); }
+            }
+        return rs;
+    };
+    auto make_phase = [&](const std::vector<uint32_t> &rs, uint16_t g0) {
+        Phase ph;
+        memset(&ph, 0, sizeof(ph));
+        ph.g0 = g0;
+        uint32_t rmask = 0;
+        for (int k = 0; k < RB; ++k) { ph.rl[k] = loc[rs[k]]; rmask |= 1u << ph.rl[k]; }
+        // lanes 0-2: tile bits 0-2 unless they are register bits (then the lowest free bit >= 3),
+        // lanes 3-4 and warps 0-1: the remaining bits ascending
+        uint32_t used = rmask;
+        int tj = 0;
+        for (uint32_t b = 0; b < 3; ++b) {
+            uint32_t pick = b;
+            if (rmask & (1u << b)) {
+                pick = 3;
+                while (used & (1u << pick)) ++pick;
+            }
+            used |= 1u << pick;
+            ph.tl[tj++] = (uint8_t)pick;
+        }
+        for (uint32_t b = 0; b < (uint32_t)TB && tj < 7; ++b)
+            if (!(used & (1u << b))) { used |= 1u << b; ph.tl[tj++] = (uint8_t)b; }
+        return ph;
+    };
+    std::vector<Phase> phases;
+    std::vector<GRec> recs;
+    std::vector<double> prm;
+    uint64_t regset = 0;
+    std::vector<uint32_t> rs;
+    auto regpos = [&](uint32_t q) -> int {
+        for (int k = 0; k < RB; ++k)
+            if (rs[k] == q) return k;
+        return -1;
+    };
+    auto addp = [&](std::initializer_list<double> v) {
+        uint16_t i = (uint16_t)prm.size();
+        for (double x : v) prm.push_back(x);
+        return i;
+    };
+    for (size_t i = 0; i < G.ops.size(); ++i) {
+        if (phases.empty() || (needq[i] >= 0 && !(regset & bit(needq[i])))) {
+            if (!phases.empty()) phases.back().g1 = (uint16_t)recs.size();
+            rs = lookahead(i, regset);
+            regset = 0;
+            for (uint32_t q : rs) regset |= bit(q);
+            phases.push_back(make_phase(rs, (uint16_t)recs.size()));
+        }
+        const KOp &k = G.ops[i];
+        const Op &o = k.op;
+        GRec r;
+        memset(&r, 0, sizeof(r));
+        double d[4];
+        if (o.kind == H) {
+            r.code = C_H + regpos(o.q0);
+        } else if (o.kind == RX || o.kind == RY) {
+            double m[8];
+            matrix_u(o, m);
+            r.code = C_U + regpos(o.q0);
+            r.pi = addp({m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7]});
+        } else if (o.kind == X || o.kind == Y) {   // in-tile
+            r.code = (o.kind == X ? C_X : C_Y) + regpos(o.q0);
+        } else if (o.kind == CX) {
+            int t = regpos(o.q1), c = regpos(o.q0);
+            if (c >= 0) r.code = C_CX + 5 * c + t;
+            else { r.code = C_TX + t; r.a = (uint8_t)o.q0; }
+        } else if (o.kind == CZ || o.kind == CP) {
+            double pr = o.kind == CZ ? -1.0 : cos(o.theta), pi = o.kind == CZ ? 0.0 : sin(o.theta);
+            int a = regpos(o.q0), b = regpos(o.q1);
+            if (a >= 0 && b >= 0) {
+                if (a > b) std::swap(a, b);
+                r.code = C_CPH + 5 * a + b;
+                r.pi = addp({pr, pi});
+            } else if (a >= 0 || b >= 0) {
+                r.code = C_TD1 + (a >= 0 ? a : b);
+                r.a = (uint8_t)(a >= 0 ? o.q1 : o.q0);
+                r.pi = addp({pr, pi});
+            } else {
+                r.code = C_TPH;
+                r.a = (uint8_t)o.q0;
+                r.b = (uint8_t)o.q1;
+                r.pi = addp({1.0, 0.0, pr, pi});
+            }
+        } else if (diag_of(o, d)) {
+            int a = regpos(o.q0);
+            const bool d0one = d[0] == 1.0 && d[1] == 0.0;
+            if (a >= 0) {
+                if (d0one) { r.code = C_D1 + a; r.pi = addp({d[2], d[3]}); }
+                else { r.code = C_D2 + a; r.pi = addp({d[0], d[1], d[2], d[3]}); }
+            } else {
+                r.code = C_TPH;
+                r.a = r.b = (uint8_t)o.q0;
+                r.pi = addp({d[0], d[1], d[2], d[3]});
+            }
+        } else {
+            throw std::runtime_error("fused planner: unsupported op kind");
+        }
+        recs.push_back(r);
+    }
+    if (phases.empty()) {
+        rs = lookahead(0, 0);
+        phases.push_back(make_phase(rs, 0));
+    }
+    phases.back().g1 = (uint16_t)recs.size();
+    if (phases.size() > (size_t)MAXPH || recs.size() > (size_t)MAXG || prm.size() > (size_t)MAXP)
+        throw std::runtime_error("fused planner: group exceeds the kernel parameter block");
+    P.nphase = (uint32_t)phases.size();
+    std::copy(phases.begin(), phases.end(), P.ph);
+    std::copy(recs.begin(), recs.end(), P.g);
+    std::copy(prm.begin(), prm.end(), P.prm);
+}
+
+static int blocks_per_sm(int prec)
+{
+    static int occ[2] = {0, 0};
+    int &o = occ[prec == 128 ? 1 : 0];
+    if (!o) {
+        size_t smem = (size_t)(1 << TB) * (prec == 128 ? 16 : 8);
+        if (prec == 128) {
+            cudaFuncSetAttribute(k_fused<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused<double>, NT, smem);
+        } else {
+            cudaFuncSetAttribute(k_fused<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused<float>, NT, smem);
+        }
+        if (o < 1) o = 1;
+    }
+    return o;
+}
+
+void FusedPlanner::execute(const std::vector<Op> &ops, Ctx &ctx)
+{
+    execute_ex(ops, ctx, nullptr, nullptr, nullptr);
+}
+
+bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitState *init, double *d_sums,
+                              bool *sums_written)
+{
+    if (sums_written) *sums_written = false;
+    std::vector<Group> groups = make_groups(ops);
+    const double s = (double)(1ull << n_) * (prec_ == 128 ? 16 : 8);
+    bool pending_init = init != nullptr;
+    if (groups.empty() && pending_init) {
+        if (!ctx.dry) launch_init_basis(ctx.psi, n_, prec_, init->index, init->re, init->im, ctx.st);
+        count(ctx, s, false);
+        xmask_ = 0;
+        return true;
+    }
+    static Built B;   // large parameter block, reused (host planner is single-threaded per call)
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const Group &G = groups[gi];
+        if (G.ops.empty() && !pending_init) {   // pure relabel
+            xmask_ ^= G.xb ^ G.xa;
+            continue;
+        }
+        build_params(G, n_, B);
+        Params &P = B.P;
+        uint64_t m_load = (pending_init ? 0 : xmask_) ^ G.xb;
+        P.xm_load = m_load;
+        P.xm_store = m_load & ~B.tile;
+        P.ntiles = 1ull << (n_ - TB);
+        P.flags = 0;
+        if (pending_init) {
+            P.flags |= F_INIT;
+            P.init_index = init->index;
+            P.init_re = init->re;
+            P.init_im = init->im;
+        }
+        double sc = 1.0;
+        int nh = 0;
+        for (auto &k : G.ops) nh += k.op.kind == H;
+        for (int i = 0; i < nh / 2; ++i) sc *= 0.5;
+        if (nh & 1) sc *= M_SQRT1_2;
+        P.scale_re = sc * G.fr;
+        P.scale_im = sc * G.fi;
+        if (P.scale_re != 1.0 || P.scale_im != 0.0) P.flags |= F_SCALE;
+        const bool last = gi + 1 == groups.size();
+        bool want = last && d_sums && B.tile == ((1ull << TB) - 1);
+        if (want) P.flags |= F_SUMS;
+        const double bytes = pending_init ? s : 2 * s;
+        if (!ctx.dry) {
+            int bps = blocks_per_sm(prec_);
+            uint64_t grid = std::min<uint64_t>(P.ntiles, (uint64_t)device_sm_count() * bps);
+            size_t smem = (size_t)(1 << TB) * (prec_ == 128 ? 16 : 8);
+            if (ctx.timer) ctx.timer->begin(ctx.st);
+            if (prec_ == 128)
+                k_fused<double><<<(unsigned)grid, NT, smem, ctx.st>>>((double2 *)ctx.psi, P, d_sums);
+            else
+                k_fused<float><<<(unsigned)grid, NT, smem, ctx.st>>>((float2 *)ctx.psi, P, d_sums);
+            if (ctx.timer) ctx.timer->end(ctx.st, bytes);
+        }
+        count(ctx, bytes, true);
+        pending_init = false;
+        xmask_ = P.xm_store ^ G.xa;
+        if (want && sums_written) *sums_written = true;
+    }
+    return true;
+}
+
+void FusedPlanner::materialize(Ctx &ctx)
+{
+    if (!xmask_) return;
+    double b = 0;
+    if (!ctx.dry) b = launch_pauli_string(ctx.psi, n_, prec_, xmask_, 0, ctx.st);
+    else b = 2.0 * (double)(1ull << n_) * (prec_ == 128 ? 16 : 8);
+    count(ctx, b, false);
+    xmask_ = 0;
+}
+
+}  // namespace tq

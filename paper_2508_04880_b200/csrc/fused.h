@@ -1,0 +1,71 @@
+// Execution context, gate-kernel timing and the K5 fused-tile planner interface.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "common.h"
+
+namespace tq {
+
+// CUDA-event brackets around gate-kernel launches (TUSQ_EXEC_PROFILE).
+class GateTimer {
+public:
+    explicit GateTimer(bool on) : on_(on) {}
+    ~GateTimer();
+    bool on() const { return on_; }
+    void begin(cudaStream_t st);
+    void end(cudaStream_t st, double bytes);
+    void flush();                 // synchronizes the recorded events and accumulates
+    uint64_t launches = 0;
+    double seconds = 0.0, bytes = 0.0;
+
+private:
+    bool on_;
+    std::vector<cudaEvent_t> a_, b_;
+    std::vector<double> by_;
+    size_t used_ = 0;
+};
+
+struct Ctx {
+    void *psi = nullptr;
+    uint32_t n = 0;
+    int prec = 128;
+    cudaStream_t st = nullptr;
+    bool dry = false;             // TUSQ_EXEC_PLAN_ONLY: count, launch nothing
+    tusq_run_stats *stats = nullptr;
+    GateTimer *timer = nullptr;
+};
+
+// Fused-tile planner (K5).  Splits an op stream into groups whose qubits fit a tile of 2^tile_bits
+// amplitudes and applies each group in one HBM sweep; keeps a pending X-relabel mask between
+// sweeps (physical index = logical index XOR mask).
+struct InitState { uint64_t index; double re, im; };   // reset target (K7 fused into the first sweep)
+
+class FusedPlanner {
+public:
+    FusedPlanner(uint32_t n, int prec, uint32_t tile_bits);
+    uint32_t tile_bits() const { return tile_bits_; }
+    bool enabled() const { return enabled_; }
+    void execute(const std::vector<Op> &ops, Ctx &ctx);
+    // init: the state is first reset to init (no load); d_sums: if the last sweep's tile is the
+    // contiguous block {0..11}, it writes per-block |amp|^2 sums (physical block order) there.
+    bool execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitState *init, double *d_sums,
+                    bool *sums_written);
+    // the logical state may be stored XOR-relabelled; materialize() clears the mask
+    uint64_t xmask() const { return xmask_; }
+    void materialize(Ctx &ctx);
+    void reset_mask() { xmask_ = 0; }
+
+private:
+    uint32_t n_;
+    int prec_;
+    uint32_t tile_bits_;
+    bool enabled_;
+    uint64_t xmask_ = 0;
+};
+
+// one kernel per gate (K1-K4); consecutive Paulis on distinct qubits merge into one K4 pass
+void execute_unfused(const std::vector<Op> &ops, Ctx &ctx);
+
+}  // namespace tq

@@ -1,0 +1,41 @@
+// Device kernel launchers (sm_100a).  All take raw device pointers and a cudaStream_t.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.h"
+
+namespace tq {
+
+// ----- K1-K4: one kernel per gate (the unfused path) -------------------------------
+// Returns the algorithmic HBM bytes the launch moves.
+double launch_gate(void *psi, uint32_t n, int prec, const Op &op, cudaStream_t st);
+// K4: a Pauli string P = prod_q P_q applied in one pass (x/z bit masks).
+double launch_pauli_string(void *psi, uint32_t n, int prec, uint64_t xmask, uint64_t zmask, cudaStream_t st);
+// K7: psi <- amp |index>
+double launch_init_basis(void *psi, uint32_t n, int prec, uint64_t index, double re, double im, cudaStream_t st);
+
+// ----- K5: fused tile kernel (see fused.cu) ------------------------------------------
+struct FusedPlan;
+double launch_fused(void *psi, uint32_t n, int prec, const FusedPlan &plan, cudaStream_t st,
+                    double *d_tile_sums);
+
+// ----- K6: sampler ---------------------------------------------------------------------
+struct SamplerWork {
+    double *d_blocks = nullptr;    // per-block |amp|^2 sums, then exclusive prefix (nb + 1)
+    uint64_t cap_blocks = 0;
+    uint32_t *d_edges = nullptr;   // edge-draw counter
+};
+// block sums of |amp|^2 over contiguous blocks of 2^block_bits amplitudes
+double launch_block_sums(const void *psi, uint32_t n, int prec, uint32_t block_bits, double *d_blocks,
+                         cudaStream_t st);
+// exclusive prefix over LOGICAL blocks of nb block sums given in PHYSICAL order (physical
+// block = logical ^ mh); d_prefix[nb] = total
+void launch_scan_blocks(const double *d_phys, double *d_prefix, uint64_t nb, uint64_t mh, cudaStream_t st);
+// draws j = 0..n_draws-1 of leaf `leaf` into d_out[j]; logical index i lives at physical i ^ xm
+double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_prefix,
+                    uint64_t n_draws, uint64_t seed, uint64_t leaf, double edge_eps, uint64_t xm, uint64_t *d_out,
+                    uint32_t *d_edges, cudaStream_t st);
+
+int device_sm_count();
+
+}  // namespace tq

@@ -1,0 +1,138 @@
+"""CPU tests of the C-ABI library: it loads, exports every declared symbol, and its host-side
+ECM / tree / scheduler logic is bit-exact with the independent oracle (no device calls)."""
+import hashlib
+import os
+import re
+
+import numpy as np
+import pytest
+
+from workloads import circuits as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="session")
+def lib():
+    from paper_2508_04880_b200 import build
+    build.build()
+    import paper_2508_04880_b200 as T
+    return T
+
+
+def test_library_exports_header_symbols(lib):
+    hdr = open(os.path.join(ROOT, "include", "tusq.h")).read()
+    declared = set(re.findall(r"\b(tusq_[a-z_]+)\s*\(", hdr))
+    assert {"tusq_build_error_tree", "tusq_run_tree", "tusq_sample"} <= declared
+    import ctypes
+    so = ctypes.CDLL(lib.LIB_PATH)
+    for name in declared:
+        assert hasattr(so, name), name
+    assert set(lib.EXPORTED) == declared
+    assert "sm_100a" in lib.version()
+
+
+def test_build_errors(lib):
+    n, ops = W.ghz(3)
+    with pytest.raises(lib.TusqError) as e:
+        lib.build_error_tree(n, ops + [W.op(W.CX, 1, 1)], 0.01, 0.01, 0, 10, 1)
+    assert e.value.status == 1 and "target" in str(e.value)
+    with pytest.raises(lib.TusqError):
+        lib.build_error_tree(n, ops + [W.op(W.H, 5)], 0.01, 0.01, 0, 10, 1)
+    with pytest.raises(lib.TusqError):
+        lib.build_error_tree(n, ops, 1.5, 0.01, 0, 10, 1)
+    with pytest.raises(lib.TusqError):
+        lib.build_error_tree(n, ops, 0.01, 0.01, 0, 0, 1)
+    with pytest.raises(lib.TusqError):
+        lib.build_error_tree(63, [], 0.01, 0.01, 0, 10, 1)
+    with pytest.raises(lib.TusqError):
+        lib.build_error_tree(n, ops, 0.01, 0.01, 0, 10, 1, beta=0)
+    with pytest.raises(lib.TusqError):
+        lib.build_error_tree(n, [(99, 0, 0, 0.0)], 0.01, 0.01, 0, 10, 1)
+
+
+def _both(lib, oracle, n, ops, p1, p2, pm, shots, seed, beta=100, prune=True):
+    a = lib.build_error_tree(n, ops, p1, p2, pm, shots, seed, beta=beta, prune=prune)
+    b = oracle.Tree(n, ops, p1, p2, pm, shots, seed, beta=beta, prune=prune)
+    return a, b
+
+
+@pytest.mark.parametrize("name", ["C1", "C2a", "C2b", "C3", "C4"])
+@pytest.mark.parametrize("seed", [1, 2])
+def test_ecm_tree_bit_exact_configs(lib, oracle, name, seed):
+    # ECM trees and tallies: bit-exact between the library's frame-based ECM and the oracle's
+    # literal-stack ECM (north star), including pruning selection, DFS order and offsets.
+    cfg = W.config(name, seed)
+    a, b = _both(lib, oracle, cfg.n, cfg.ops, cfg.noise.p1, cfg.noise.p2, cfg.noise.p_meas, cfg.shots, seed)
+    sa, sb = a.serialize(), b.serialize()
+    assert len(sa) == len(sb)
+    assert hashlib.sha256(sa).hexdigest() == hashlib.sha256(sb).hexdigest()
+
+
+def test_ecm_bit_exact_random(lib, oracle):
+    rng = np.random.default_rng(21)
+    for trial in range(60):
+        n = int(rng.integers(1, 7))
+        ops = W.random_circuit(rng, n, int(rng.integers(1, 40)))
+        p1, p2, pm = [float(x) for x in rng.choice([0.0, 0.01, 0.1, 0.4], size=3)]
+        shots = int(rng.integers(1, 3000))
+        seed = int(rng.integers(0, 1 << 62))
+        beta = int(rng.integers(1, 30))
+        prune = bool(rng.integers(0, 2))
+        a, b = _both(lib, oracle, n, ops, p1, p2, pm, shots, seed, beta, prune)
+        assert a.serialize() == b.serialize(), (trial, n, ops, p1, p2, pm, shots, seed, beta, prune)
+
+
+def _events(ops, tr):
+    L = len(ops)
+    ev = []
+    k = 0
+    for pos in range(L + 1):
+        while k < len(tr) and tr[k][0] == pos:
+            ev.append(("P", tr[k][1], tr[k][2]))
+            k += 1
+        if pos < L:
+            ev.append(("G", pos))
+    return ev
+
+
+def test_tree_info_matches_explicit_trie(lib):
+    # |E| = number of ops on the edges of the prefix trie of leaf event streams;
+    # DFTT fwd + inv = 2|E| - depth(last leaf) (P:329 counts every edge twice; the path to the
+    # last leaf is never uncomputed); naive = sum of leaf lengths (P:333 T_naive).
+    for name in ["C1", "C2a", "C3"]:
+        cfg = W.config(name)
+        t = lib.build_error_tree(cfg.n, cfg.ops, cfg.noise.p1, cfg.noise.p2, cfg.noise.p_meas, cfg.shots, cfg.seed)
+        info = t.info()
+        streams = [_events(cfg.ops, t.leaf(l)[0]) for l in range(info["n_leaves"])]
+        trie = set()
+        for s in streams:
+            for d in range(1, len(s) + 1):
+                trie.add(tuple(s[:d]))
+        assert info["edges"] == len(trie)
+        assert info["dftt_ops"] == 2 * info["edges"] - len(streams[-1])
+        assert info["naive_ops"] == sum(len(s) for s in streams)
+        assert info["S1"] >= info["S2"] >= info["S3"] >= info["n_leaves"]
+
+
+def test_dftt_closed_forms_full_tree():
+    # full b-ary tree of height h: |E| = b(b^h - 1)/(b - 1), N_l = b^h = (1 - 1/b)|E| + 1,
+    # h = log_b((b-1)|E| + b) - 1, T_dftt = 2|E|, T_naive = N_l h.
+    import math
+    for b, h, E, Nl in [(4, 2, 20, 16), (2, 5, 62, 32)]:
+        assert b * (b ** h - 1) // (b - 1) == E
+        assert (1 - 1 / b) * E + 1 == Nl
+        assert abs(math.log((b - 1) * E + b, b) - 1 - h) < 1e-12
+        # explicit DFS over the full tree: every edge traversed twice
+        leaves = [tuple((i // b ** j) % b for j in range(h)) for i in range(b ** h)]
+        trie = {lf[:d] for lf in leaves for d in range(1, h + 1)}
+        assert len(trie) == E and len(leaves) == Nl
+
+
+def test_partition_contiguous_and_balanced(lib):
+    cfg = W.config("C3")
+    t = lib.build_error_tree(cfg.n, cfg.ops, cfg.noise.p1, cfg.noise.p2, cfg.noise.p_meas, cfg.shots, cfg.seed)
+    nl = t.n_leaves
+    for nr in (1, 2, 4, 8):
+        b = t.partition(nr)
+        assert b[0] == 0 and b[-1] == nl and np.all(np.diff(b.astype(np.int64)) >= 0)
