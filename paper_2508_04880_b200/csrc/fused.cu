@@ -22,6 +22,8 @@
 //   - the last sweep before sampling can emit per-4096-block |amp|^2 sums (K6 epilogue).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -37,7 +39,7 @@ constexpr int NR = 32;     // amplitudes per thread
 constexpr int NT = 128;    // threads per CTA
 constexpr int MAXPH = 24;
 constexpr int MAXG = 400;
-constexpr int MAXP = 900;
+constexpr int MAXP = 1600;
 
 enum Code : uint16_t {
     C_H = 0,      // +r      unscaled butterfly
@@ -51,13 +53,23 @@ enum Code : uint16_t {
     C_TX = 80,    // +t      if pred(q): X on reg t
     C_TD1 = 85,   // +r      if pred(q): bit 1 of reg r *= p
     C_TPH = 90,   //         all *= pred(q0)&pred(q1) ? p1 : p0 (4 params)
-    C_N = 91
+    C_DK = 91,    // +mask   a[r] *= tab[pext(r, mask)]  (2 * 2^popc(mask) params)
+    C_N = 123
 };
+
+__host__ __device__ constexpr int pext5(int r, int m)
+{
+    int o = 0, k = 0;
+    for (int b = 0; b < 5; ++b)
+        if ((m >> b) & 1) { o |= ((r >> b) & 1) << k; ++k; }
+    return o;
+}
 
 struct Phase {
     uint16_t g0, g1;      // gate range
     uint8_t rl[RB];       // tile-local bit of each register bit
     uint8_t tl[7];        // tile-local bit of each thread bit (lanes 0-4, warps 0-1)
+    uint16_t so[NR];      // tile-local index contribution of register r (host-computed)
 };
 
 struct GRec {
@@ -77,7 +89,10 @@ struct Params {
     uint64_t ntiles;
     uint32_t flags, nphase;
     uint8_t qs[TB];               // tile-local bit b <-> global qubit qs[b] (ascending)
-    uint32_t _pad;
+    uint32_t rx;                  // register bits where xm_load is set: fixed up by X after the load
+    uint64_t regm_load;           // global mask of the phase-0 register qubits
+    uint64_t gl[NR];              // phase 0: global element offset of register r (additive)
+    uint64_t gs[NR];              // last phase: global element offset of register r (additive)
     Phase ph[MAXPH];
     GRec g[MAXG];
     double prm[MAXP];
@@ -191,6 +206,16 @@ __device__ __forceinline__ void g_cph(V (&a)[NR], R pr, R pi)
         if ((i & (1 << A)) && (i & (1 << B))) a[i] = mulc(a[i], pr, pi);
 }
 
+template <int M, typename V, typename R>
+__device__ __forceinline__ void g_dk(V (&a)[NR], const double *tab)
+{
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+        const int idx = pext5(i, M);
+        a[i] = mulc(a[i], (R)tab[2 * idx], (R)tab[2 * idx + 1]);
+    }
+}
+
 template <typename V, typename R>
 __device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const double *prm, uint64_t lbase)
 {
@@ -243,6 +268,12 @@ __device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const doub
     TQ_CP(1, 2) TQ_CP(1, 3) TQ_CP(1, 4)
     TQ_CP(2, 3) TQ_CP(2, 4)
     TQ_CP(3, 4)
+#define TQ_DK(m) case C_DK + m: g_dk<m, V, R>(a, p); break;
+    TQ_DK(1) TQ_DK(2) TQ_DK(3) TQ_DK(4) TQ_DK(5) TQ_DK(6) TQ_DK(7) TQ_DK(8) TQ_DK(9) TQ_DK(10)
+    TQ_DK(11) TQ_DK(12) TQ_DK(13) TQ_DK(14) TQ_DK(15) TQ_DK(16) TQ_DK(17) TQ_DK(18) TQ_DK(19) TQ_DK(20)
+    TQ_DK(21) TQ_DK(22) TQ_DK(23) TQ_DK(24) TQ_DK(25) TQ_DK(26) TQ_DK(27) TQ_DK(28) TQ_DK(29) TQ_DK(30)
+    TQ_DK(31)
+#undef TQ_DK
     default: {
         const bool pa = (lbase >> g.a) & 1;
         if (g.code == C_TPH) {
@@ -302,36 +333,34 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
 #pragma unroll
         for (int b = 0; b < TB; ++b) base = ins0(base, P.qs[b]);
 
-        // ---- phase 0 layout: global offsets of thread bits and register bits
-        uint64_t gthr = 0, greg[RB];
+        // ---- phase 0 layout: global offset of this thread's bits; register offsets come from
+        // the parameter block (constant bank), added to one base pointer
+        uint64_t gthr = 0;
         {
             const Phase &p0 = P.ph[0];
 #pragma unroll
             for (int j = 0; j < 7; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[p0.tl[j]];
-#pragma unroll
-            for (int k = 0; k < RB; ++k) greg[k] = 1ull << P.qs[p0.rl[k]];
         }
         if (P.flags & F_INIT) {
             const uint64_t lt = (base | gthr) ^ P.xm_load;
 #pragma unroll
             for (int r = 0; r < NR; ++r) {
-                uint64_t o = 0;
-#pragma unroll
-                for (int k = 0; k < RB; ++k)
-                    if (r & (1 << k)) o ^= greg[k];
-                const bool hit = (lt ^ o) == P.init_index;
+                const bool hit = (lt ^ P.gl[r]) == P.init_index;
                 a[r].x = hit ? (R)P.init_re : R(0);
                 a[r].y = hit ? (R)P.init_im : R(0);
             }
         } else {
-            const uint64_t pld = (base | gthr) ^ P.xm_load;
+            // physical = logical ^ xm_load; register-position bits of the mask are applied as
+            // in-register X after an additive load
+            const V *p0 = psi + (((base | gthr) ^ P.xm_load) & ~P.regm_load);
 #pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                uint64_t o = 0;
-#pragma unroll
-                for (int k = 0; k < RB; ++k)
-                    if (r & (1 << k)) o ^= greg[k];
-                a[r] = __ldcs(psi + (pld ^ o));
+            for (int r = 0; r < NR; ++r) a[r] = __ldcs(p0 + P.gl[r]);
+            if (P.rx) {
+                if (P.rx & 1) g_x<0>(a);
+                if (P.rx & 2) g_x<1>(a);
+                if (P.rx & 4) g_x<2>(a);
+                if (P.rx & 8) g_x<3>(a);
+                if (P.rx & 16) g_x<4>(a);
             }
         }
 
@@ -340,13 +369,11 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
             if (ph > 0) {
                 // transpose registers from the previous layout to this one through shared memory
                 const Phase &prv = P.ph[ph - 1];
-                uint32_t tt = 0, rb[RB];
+                uint32_t tt = 0;
 #pragma unroll
                 for (int j = 0; j < 7; ++j) tt |= ((tid >> j) & 1u) << prv.tl[j];
-#pragma unroll
-                for (int k = 0; k < RB; ++k) rb[k] = 1u << prv.rl[k];
                 __syncthreads();
-#define TQ_ST(r) sm[swz(tt | roff32<r>(rb))] = a[r];
+#define TQ_ST(r) sm[swz(tt | prv.so[r])] = a[r];
                 TQ_ST(0) TQ_ST(1) TQ_ST(2) TQ_ST(3) TQ_ST(4) TQ_ST(5) TQ_ST(6) TQ_ST(7)
                 TQ_ST(8) TQ_ST(9) TQ_ST(10) TQ_ST(11) TQ_ST(12) TQ_ST(13) TQ_ST(14) TQ_ST(15)
                 TQ_ST(16) TQ_ST(17) TQ_ST(18) TQ_ST(19) TQ_ST(20) TQ_ST(21) TQ_ST(22) TQ_ST(23)
@@ -356,9 +383,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 tt = 0;
 #pragma unroll
                 for (int j = 0; j < 7; ++j) tt |= ((tid >> j) & 1u) << cur.tl[j];
-#pragma unroll
-                for (int k = 0; k < RB; ++k) rb[k] = 1u << cur.rl[k];
-#define TQ_LD(r) a[r] = sm[swz(tt | roff32<r>(rb))];
+#define TQ_LD(r) a[r] = sm[swz(tt | cur.so[r])];
                 TQ_LD(0) TQ_LD(1) TQ_LD(2) TQ_LD(3) TQ_LD(4) TQ_LD(5) TQ_LD(6) TQ_LD(7)
                 TQ_LD(8) TQ_LD(9) TQ_LD(10) TQ_LD(11) TQ_LD(12) TQ_LD(13) TQ_LD(14) TQ_LD(15)
                 TQ_LD(16) TQ_LD(17) TQ_LD(18) TQ_LD(19) TQ_LD(20) TQ_LD(21) TQ_LD(22) TQ_LD(23)
@@ -377,8 +402,6 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
         gthr = 0;
 #pragma unroll
         for (int j = 0; j < 7; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[last.tl[j]];
-#pragma unroll
-        for (int k = 0; k < RB; ++k) greg[k] = 1ull << P.qs[last.rl[k]];
         if (P.flags & F_SCALE) {
             const R sr = (R)P.scale_re, si = (R)P.scale_im;
             if (si == R(0)) {
@@ -389,15 +412,10 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 for (int r = 0; r < NR; ++r) a[r] = mulc(a[r], sr, si);
             }
         }
-        const uint64_t pst = (base | gthr) ^ P.xm_store;
+        // xm_store has no tile bits: register offsets are additive
+        V *q0 = psi + ((base | gthr) ^ P.xm_store);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
-            uint64_t o = 0;
-#pragma unroll
-            for (int k = 0; k < RB; ++k)
-                if (r & (1 << k)) o ^= greg[k];
-            __stcs(psi + (pst ^ o), a[r]);
-        }
+        for (int r = 0; r < NR; ++r) __stcs(q0 + P.gs[r], a[r]);
         if (P.flags & F_SUMS) {
             double s = 0.0;
 #pragma unroll
@@ -698,8 +716,16 @@ static void build_params(const Group &G, uint32_t n, Built &B)
     auto lookahead = [&](size_t from, uint64_t keep) {
         std::vector<uint32_t> rs;
         uint64_t have = 0;
-        for (size_t i = from; i < G.ops.size() && rs.size() < (size_t)RB; ++i)
-            if (needq[i] >= 0 && !(have & bit(needq[i]))) { have |= bit(needq[i]); rs.push_back(needq[i]); }
+        // upcoming qubits in order of first appearance: exchange targets (hard), and the controls /
+        // diagonal qubits next to them (soft: in registers they avoid predicated whole-register work
+        // and let monomial folding see the whole run)
+        for (size_t i = from; i < G.ops.size() && rs.size() < (size_t)RB; ++i) {
+            const Op &o = G.ops[i].op;
+            uint32_t cand[2] = {needq[i] >= 0 ? (uint32_t)needq[i] : o.q0, o.q0};
+            if (two_qubit(o.kind) && needq[i] < 0) cand[1] = o.q1;
+            for (uint32_t q : cand)
+                if (rs.size() < (size_t)RB && !(have & bit(q)) && (tile & bit(q))) { have |= bit(q); rs.push_back(q); }
+        }
         // fill: keep previous register qubits, then tile qubits touched by diagonals, then any >= 3
         for (uint64_t m = keep; m && rs.size() < (size_t)RB; m &= m - 1) {
             uint32_t q = __builtin_ctzll(m);
@@ -734,6 +760,12 @@ static void build_params(const Group &G, uint32_t n, Built &B)
         }
         for (uint32_t b = 0; b < (uint32_t)TB && tj < 7; ++b)
             if (!(used & (1u << b))) { used |= 1u << b; ph.tl[tj++] = (uint8_t)b; }
+        for (int r = 0; r < NR; ++r) {
+            uint32_t o = 0;
+            for (int k = 0; k < RB; ++k)
+                if (r & (1 << k)) o |= 1u << ph.rl[k];
+            ph.so[r] = (uint16_t)o;
+        }
         return ph;
     };
     std::vector<Phase> phases;
@@ -751,6 +783,81 @@ static void build_params(const Group &G, uint32_t n, Built &B)
         for (double x : v) prm.push_back(x);
         return i;
     };
+    // Monomial folding: a run of CX / diagonal / in-register X,Y gates on register qubits whose
+    // net permutation is the identity is one diagonal: a[r] *= tab[pext(r, mask)].  (The CX+T
+    // core of a Toffoli, P:457's Cuccaro adder, is such a run.)  Tables are built by simulating
+    // the run on the 32 register patterns in double.
+    auto classical = [&](size_t j) -> bool {
+        const KOp &k = G.ops[j];
+        const Op &o = k.op;
+        auto inreg = [&](uint32_t q) { return (regset & bit(q)) != 0; };
+        double d[4];
+        if (o.kind == CX || o.kind == CZ || o.kind == CP) return inreg(o.q0) && inreg(o.q1);
+        if ((o.kind == X || o.kind == Y) && k.in_tile_xy) return inreg(o.q0);
+        if (diag_of(o, d)) return inreg(o.q0);
+        return false;
+    };
+    auto try_fold = [&](size_t i, size_t &fe, uint32_t &fmask, std::vector<double> &tab) -> bool {
+        uint8_t perm[NR];
+        double pr[NR], pi[NR];
+        for (int x = 0; x < NR; ++x) { perm[x] = (uint8_t)x; pr[x] = 1.0; pi[x] = 0.0; }
+        uint32_t mask = 0;
+        size_t best = i;
+        uint32_t best_mask = 0;
+        double br[NR], bi[NR];
+        for (size_t j = i; j < G.ops.size() && classical(j); ++j) {
+            if (needq[j] >= 0 && !(regset & bit(needq[j]))) break;
+            const Op &o = G.ops[j].op;
+            const int a = regpos(o.q0), b = two_qubit(o.kind) ? regpos(o.q1) : -1;
+            mask |= 1u << a;
+            if (b >= 0) mask |= 1u << b;
+            double d[4];
+            const bool dg = diag_of(o, d);
+            for (int x = 0; x < NR; ++x) {
+                uint32_t y = perm[x];
+                double fr = 1.0, fi = 0.0;
+                if (o.kind == CX) { if ((y >> a) & 1) y ^= 1u << b; }
+                else if (o.kind == X) { y ^= 1u << a; }
+                else if (o.kind == Y) { fr = 0.0; fi = ((y >> a) & 1) ? -1.0 : 1.0; y ^= 1u << a; }
+                else if (o.kind == CZ || o.kind == CP) {
+                    if (((y >> a) & 1) && ((y >> b) & 1)) {
+                        fr = o.kind == CZ ? -1.0 : cos(o.theta);
+                        fi = o.kind == CZ ? 0.0 : sin(o.theta);
+                    }
+                } else if (dg) {
+                    const bool s = (y >> a) & 1;
+                    fr = s ? d[2] : d[0];
+                    fi = s ? d[3] : d[1];
+                }
+                const double nr = pr[x] * fr - pi[x] * fi, ni = pr[x] * fi + pi[x] * fr;
+                pr[x] = nr; pi[x] = ni;
+                perm[x] = (uint8_t)y;
+            }
+            bool ident = true;
+            for (int x = 0; x < NR && ident; ++x) ident = perm[x] == x;
+            if (ident) {
+                best = j + 1;
+                best_mask = mask;
+                memcpy(br, pr, sizeof(br));
+                memcpy(bi, pi, sizeof(bi));
+            }
+        }
+        if (best < i + 2) return false;
+        fe = best;
+        fmask = best_mask;
+        tab.clear();
+        const int k = __builtin_popcount(fmask);
+        for (int idx = 0; idx < (1 << k); ++idx) {
+            uint32_t x = 0;
+            int t = 0;
+            for (int b = 0; b < RB; ++b)
+                if (fmask & (1u << b)) { if ((idx >> t) & 1) x |= 1u << b; ++t; }
+            tab.push_back(br[x]);
+            tab.push_back(bi[x]);
+        }
+        return true;
+    };
+    std::vector<double> ftab;
     for (size_t i = 0; i < G.ops.size(); ++i) {
         if (phases.empty() || (needq[i] >= 0 && !(regset & bit(needq[i])))) {
             if (!phases.empty()) phases.back().g1 = (uint16_t)recs.size();
@@ -758,6 +865,20 @@ static void build_params(const Group &G, uint32_t n, Built &B)
             regset = 0;
             for (uint32_t q : rs) regset |= bit(q);
             phases.push_back(make_phase(rs, (uint16_t)recs.size()));
+        }
+        {
+            size_t fe = i;
+            uint32_t fmask = 0;
+            if (try_fold(i, fe, fmask, ftab)) {
+                GRec r;
+                memset(&r, 0, sizeof(r));
+                r.code = C_DK + fmask;
+                r.pi = (uint16_t)prm.size();
+                prm.insert(prm.end(), ftab.begin(), ftab.end());
+                recs.push_back(r);
+                i = fe - 1;
+                continue;
+            }
         }
         const KOp &k = G.ops[i];
         const Op &o = k.op;
@@ -818,6 +939,23 @@ static void build_params(const Group &G, uint32_t n, Built &B)
     if (phases.size() > (size_t)MAXPH || recs.size() > (size_t)MAXG || prm.size() > (size_t)MAXP)
         throw std::runtime_error("fused planner: group exceeds the kernel parameter block");
     P.nphase = (uint32_t)phases.size();
+    static const bool dbg = getenv("TUSQ_DEBUG_PLAN") != nullptr;
+    if (dbg) {
+        fprintf(stderr, "[plan] ops %zu recs %zu phases %zu prm %zu tile %#llx\n", G.ops.size(), recs.size(),
+                phases.size(), prm.size(), (unsigned long long)tile);
+        if (getenv("TUSQ_DEBUG_PLAN")[0] == '2') {
+            for (auto &k : G.ops) fprintf(stderr, " %u(%u,%u)", k.op.kind, k.op.q0, k.op.q1);
+            fprintf(stderr, "\n  codes:");
+            for (auto &r : recs) fprintf(stderr, " %u", r.code);
+            fprintf(stderr, "\n  phases:");
+            for (auto &ph : phases) {
+                fprintf(stderr, " [g%u-%u regs", ph.g0, ph.g1);
+                for (int k = 0; k < RB; ++k) fprintf(stderr, " %u", P.qs[ph.rl[k]]);
+                fprintf(stderr, "]");
+            }
+            fprintf(stderr, "\n");
+        }
+    }
     std::copy(phases.begin(), phases.end(), P.ph);
     std::copy(recs.begin(), recs.end(), P.g);
     std::copy(prm.begin(), prm.end(), P.prm);
@@ -871,6 +1009,22 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         uint64_t m_load = (pending_init ? 0 : xmask_) ^ G.xb;
         P.xm_load = m_load;
         P.xm_store = m_load & ~B.tile;
+        {
+            const Phase &f = P.ph[0], &l = P.ph[P.nphase - 1];
+            P.regm_load = 0;
+            P.rx = 0;
+            for (int k = 0; k < RB; ++k) {
+                P.regm_load |= bit(P.qs[f.rl[k]]);
+                if (m_load & bit(P.qs[f.rl[k]])) P.rx |= 1u << k;
+            }
+            for (int r = 0; r < NR; ++r) {
+                uint64_t a = 0, b = 0;
+                for (int k = 0; k < RB; ++k)
+                    if (r & (1 << k)) { a |= bit(P.qs[f.rl[k]]); b |= bit(P.qs[l.rl[k]]); }
+                P.gl[r] = a;
+                P.gs[r] = b;
+            }
+        }
         P.ntiles = 1ull << (n_ - TB);
         P.flags = 0;
         if (pending_init) {

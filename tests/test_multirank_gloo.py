@@ -1,0 +1,62 @@
+"""World-size-2 gloo test of the replica multi-GPU path on CPU: identical trees on both ranks,
+contiguous cost-balanced leaf ranges, and the SUM reduction of disjoint slot arrays reproducing
+the single-rank result bit for bit.  The device run of each range is stood in for by the oracle
+(test infrastructure) because this container has no GPU; the GPU tests cover run_tree itself."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from workloads import circuits as W
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, out_dir):
+    import torch.distributed as dist
+
+    import paper_2508_04880_b200 as T
+    from oracle import oracle as O
+    from paper_2508_04880_b200 import dist as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = W.config(name)
+    nz = cfg.noise
+    tree = T.build_error_tree(cfg.n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
+    ot = O.Tree.from_config(cfg)
+
+    def run_range(b, e):
+        out = np.zeros(cfg.shots, dtype=np.uint64)
+        for l in range(b, e):
+            _, cnt, off = ot.leaf(l)
+            k, _ = ot.sample_leaf(ot.replay_leaf(l), l)
+            out[off:off + cnt] = k
+        return out
+
+    slots, (lb, le) = D.run_tree_distributed(tree, run_range=run_range, device="cpu")
+    np.save(os.path.join(out_dir, f"slots{rank}.npy"), slots)
+    np.save(os.path.join(out_dir, f"range{rank}.npy"), np.array([lb, le]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2a"])
+def test_gloo_world2_matches_single_rank(tmp_path, oracle, name):
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, name, str(tmp_path)), nprocs=2, join=True)
+    s0 = np.load(tmp_path / "slots0.npy")
+    s1 = np.load(tmp_path / "slots1.npy")
+    r0, r1 = np.load(tmp_path / "range0.npy"), np.load(tmp_path / "range1.npy")
+    assert r0[0] == 0 and r0[1] == r1[0] and r1[1] > r1[0]
+    assert np.array_equal(s0, s1)
+    ref, _ = oracle.Tree.from_config(W.config(name)).run()
+    assert np.array_equal(s0, ref)
