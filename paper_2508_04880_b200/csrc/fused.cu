@@ -567,8 +567,10 @@ FusedPlanner::FusedPlanner(uint32_t n, int prec, uint32_t tile_bits)
 }
 
 // ---- group formation (greedy over the op stream) --------------------------------------
-static std::vector<Group> make_groups(const std::vector<Op> &ops)
+static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
 {
+    // strict: every qubit an op touches (controls, diagonals) must join the tile, so whole runs
+    // stay in registers and fold; otherwise they join only while there is room
     const uint64_t low = 7;   // qubits 0,1,2 are always tile qubits
     std::vector<Group> groups;
     Group g;
@@ -606,21 +608,25 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops)
         if (o.kind == I) continue;
         const uint64_t qm = op_qubits(o);
         // requirements of this op on the group's tile set
+        const bool xy = (o.kind == X || o.kind == Y);
         uint64_t need = 0;
         if (is_exchange(o)) need |= bit(o.q0);
         if (o.kind == CX) need |= bit(o.q1);
+        if (strict && !xy) need |= qm;
         // a pending X/Y on a qubit this op touches must be applied in registers
         for (uint64_t m = qm; m; m &= m - 1) {
             uint32_t q = __builtin_ctzll(m);
             if (pending[q] >= 0) need |= bit(q);
         }
-        const bool xy = (o.kind == X || o.kind == Y);
         const bool fits = popc_hi(g.tilemask | need) <= TB - 3 && g.ops.size() + 1 < (size_t)MAXG - 8;
         if (!fits) close();
         // re-evaluate after a possible close (pending cleared)
         need = 0;
         if (is_exchange(o)) need |= bit(o.q0);
         if (o.kind == CX) need |= bit(o.q1);
+        if (strict && !xy) need |= qm;
+        // soft: controls / diagonal qubits join the tile while there is room (never close a group)
+        if (!xy && popc_hi(g.tilemask | need | qm) <= TB - 3) need |= qm;
         for (uint64_t m = qm; m; m &= m - 1) {
             uint32_t q = __builtin_ctzll(m);
             if (pending[q] >= 0) {
@@ -988,7 +994,15 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                               bool *sums_written)
 {
     if (sums_written) *sums_written = false;
-    std::vector<Group> groups = make_groups(ops);
+    // strict grouping when it costs (almost) no extra sweeps -- e.g. ripple-carry ladders --
+    // otherwise tile membership for controls/diagonals only while there is room (e.g. QFT)
+    static const char *mode_env = getenv("TUSQ_TILE_MODE");
+    static const int mode = !mode_env ? 0 : (mode_env[0] == 's' ? 1 : mode_env[0] == 'l' ? 2 : 0);
+    std::vector<Group> groups = make_groups(ops, mode == 1);
+    if (mode == 0) {
+        std::vector<Group> g2 = make_groups(ops, true);
+        if (g2.size() * 100 <= groups.size() * 105) groups.swap(g2);
+    }
     const double s = (double)(1ull << n_) * (prec_ == 128 ? 16 : 8);
     bool pending_init = init != nullptr;
     if (groups.empty() && pending_init) {
