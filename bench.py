@@ -112,6 +112,12 @@ def cpu_oracle_rate(cfg, max_seconds: float = 20.0):
     return dt, cores, desc
 
 
+def workload_desc(cfg) -> str:
+    nz = cfg.noise
+    return (f"{cfg.name}: {cfg.n}q Cuccaro adder (L={len(cfg.ops)}), depolarizing p1={nz.p1} p2={nz.p2}"
+            + (f" p_meas={nz.p_meas}" if nz.p_meas else "") + f", {cfg.shots} shots, seed {cfg.seed}, alpha 1/100, beta 100")
+
+
 def run_reference(args, rank, world):
     """The CPU oracle (test infrastructure) timed on the host cores on this workload."""
     if rank != 0:
@@ -134,8 +140,8 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.n}q Cuccaro adder, p1={cfg.noise.p1} p2={cfg.noise.p2}, "
-                                   f"{cfg.shots} shots, seed {cfg.seed}", "extrapolated": True},
+            "config": {"workload": workload_desc(cfg), "extrapolated": True,
+                       "projection": "oracle ECM s + (oracle s per gate application) x naive gate applications"},
             "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -244,8 +250,7 @@ def main():
         "ms_per_step": t_dev_max * 1e3 / (1 if args.full else args.steps),
         "higher_is_better": False, "scaling": "strong" if args.full else "weak", "vs_baseline": None,
         "dtype": "c128" if prec == 128 else "c64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {n}q Cuccaro adder (L={len(cfg.ops)}), depolarizing p1={nz.p1} "
-                               f"p2={nz.p2}, {cfg.shots} shots, seed {cfg.seed}, alpha 1/100, beta 100",
+        "config": {"workload": workload_desc(cfg),
                    "leaves": info["n_leaves"], "leaves_per_step": B, "rank_leaves": [lb, le],
                    "extrapolated": not args.full,
                    "projection": "ECM s + rank plan bytes / measured bytes-per-s over the timed steps (max over ranks)",

@@ -117,17 +117,79 @@ __device__ __forceinline__ V mulc(V a, R pr, R pi)
     return r;
 }
 
+// a *= (pr + i pi) in place.  Written in PTX with read-write operands so the results stay in a's
+// registers (C++ lets the compiler allocate fresh registers and copy back at the switch join).
+__device__ __forceinline__ void cmul_ip(double2 &a, double pr, double pi)
+{
+    asm volatile("{\n\t.reg .f64 u, v;\n\t"
+                 "mul.f64 u, %1, %3;\n\t"
+                 "mul.f64 v, %0, %3;\n\t"
+                 "neg.f64 u, u;\n\t"
+                 "fma.rn.f64 %0, %0, %2, u;\n\t"
+                 "fma.rn.f64 %1, %1, %2, v;\n\t}"
+                 : "+d"(a.x), "+d"(a.y) : "d"(pr), "d"(pi));
+}
+__device__ __forceinline__ void cmul_ip(float2 &a, float pr, float pi)
+{
+    asm volatile("{\n\t.reg .f32 u, v;\n\t"
+                 "mul.f32 u, %1, %3;\n\t"
+                 "mul.f32 v, %0, %3;\n\t"
+                 "neg.f32 u, u;\n\t"
+                 "fma.rn.f32 %0, %0, %2, u;\n\t"
+                 "fma.rn.f32 %1, %1, %2, v;\n\t}"
+                 : "+f"(a.x), "+f"(a.y) : "f"(pr), "f"(pi));
+}
+// unscaled butterfly in place: y <- x - y, x <- 2x - y  (= x + y up to one rounding)
+__device__ __forceinline__ void bfly_ip(double2 &x, double2 &y)
+{
+    asm volatile("{\n\t.reg .f64 s, t;\n\t"
+                 "sub.rn.f64 %2, %0, %2;\n\tsub.rn.f64 %3, %1, %3;\n\t"
+                 "neg.f64 s, %2;\n\tneg.f64 t, %3;\n\t"
+                 "fma.rn.f64 %0, 0d4000000000000000, %0, s;\n\tfma.rn.f64 %1, 0d4000000000000000, %1, t;\n\t}"
+                 : "+d"(x.x), "+d"(x.y), "+d"(y.x), "+d"(y.y));
+}
+__device__ __forceinline__ void bfly_ip(float2 &x, float2 &y)
+{
+    asm volatile("{\n\t.reg .f32 s, t;\n\t"
+                 "sub.rn.f32 %2, %0, %2;\n\tsub.rn.f32 %3, %1, %3;\n\t"
+                 "neg.f32 s, %2;\n\tneg.f32 t, %3;\n\t"
+                 "fma.rn.f32 %0, 0f40000000, %0, s;\n\tfma.rn.f32 %1, 0f40000000, %1, t;\n\t}"
+                 : "+f"(x.x), "+f"(x.y), "+f"(y.x), "+f"(y.y));
+}
+
 // ---------------------------------------------------------------- register gate ops
+// Every op updates its registers IN PLACE (no result lands in a fresh register): the gate loop
+// is a switch inside a loop over 128 live registers, and any renaming inside a case costs a
+// copy of the whole amplitude set at the join (measured: 66 % of executed instructions were
+// moves before this).  Swaps are explicit XOR-swaps in PTX so that ptxas cannot rename them.
+__device__ __forceinline__ void xswap(double &x, double &y)
+{
+    long long a = __double_as_longlong(x), b = __double_as_longlong(y);
+    asm volatile("xor.b64 %0, %0, %1;\n\txor.b64 %1, %1, %0;\n\txor.b64 %0, %0, %1;" : "+l"(a), "+l"(b));
+    x = __longlong_as_double(a);
+    y = __longlong_as_double(b);
+}
+__device__ __forceinline__ void xswap(float &x, float &y)
+{
+    int a = __float_as_int(x), b = __float_as_int(y);
+    asm volatile("xor.b32 %0, %0, %1;\n\txor.b32 %1, %1, %0;\n\txor.b32 %0, %0, %1;" : "+r"(a), "+r"(b));
+    x = __int_as_float(a);
+    y = __int_as_float(b);
+}
+template <typename V>
+__device__ __forceinline__ void vswap(V &x, V &y)
+{
+    xswap(x.x, y.x);
+    xswap(x.y, y.y);
+}
+
 template <int B, typename V>
 __device__ __forceinline__ void g_h(V (&a)[NR])
 {
+    // unscaled butterfly (x, y) -> (x + y, x - y), in place: y <- x - y, x <- 2x - y
 #pragma unroll
     for (int i = 0; i < NR; ++i)
-        if (!(i & (1 << B))) {
-            V x = a[i], y = a[i | (1 << B)];
-            a[i].x = x.x + y.x; a[i].y = x.y + y.y;
-            a[i | (1 << B)].x = x.x - y.x; a[i | (1 << B)].y = x.y - y.y;
-        }
+        if (!(i & (1 << B))) bfly_ip(a[i], a[i | (1 << B)]);
 }
 
 template <int B, typename V, typename R>
@@ -151,11 +213,7 @@ __device__ __forceinline__ void g_x(V (&a)[NR])
 {
 #pragma unroll
     for (int i = 0; i < NR; ++i)
-        if (!(i & (1 << B))) {
-            V x = a[i];
-            a[i] = a[i | (1 << B)];
-            a[i | (1 << B)] = x;
-        }
+        if (!(i & (1 << B))) vswap(a[i], a[i | (1 << B)]);
 }
 
 template <int B, typename V>
@@ -176,14 +234,17 @@ __device__ __forceinline__ void g_d1(V (&a)[NR], R pr, R pi)
 {
 #pragma unroll
     for (int i = 0; i < NR; ++i)
-        if (i & (1 << B)) a[i] = mulc(a[i], pr, pi);
+        if (i & (1 << B)) cmul_ip(a[i], pr, pi);
 }
 
 template <int B, typename V, typename R>
 __device__ __forceinline__ void g_d2(V (&a)[NR], const double *p)
 {
 #pragma unroll
-    for (int i = 0; i < NR; ++i) a[i] = (i & (1 << B)) ? mulc(a[i], (R)p[2], (R)p[3]) : mulc(a[i], (R)p[0], (R)p[1]);
+    for (int i = 0; i < NR; ++i) {
+        if (i & (1 << B)) cmul_ip(a[i], (R)p[2], (R)p[3]);
+        else cmul_ip(a[i], (R)p[0], (R)p[1]);
+    }
 }
 
 template <int C, int T, typename V>
@@ -191,11 +252,7 @@ __device__ __forceinline__ void g_cx(V (&a)[NR])
 {
 #pragma unroll
     for (int i = 0; i < NR; ++i)
-        if ((i & (1 << C)) && !(i & (1 << T))) {
-            V x = a[i];
-            a[i] = a[i | (1 << T)];
-            a[i | (1 << T)] = x;
-        }
+        if ((i & (1 << C)) && !(i & (1 << T))) vswap(a[i], a[i | (1 << T)]);
 }
 
 template <int A, int B, typename V, typename R>
@@ -203,7 +260,7 @@ __device__ __forceinline__ void g_cph(V (&a)[NR], R pr, R pi)
 {
 #pragma unroll
     for (int i = 0; i < NR; ++i)
-        if ((i & (1 << A)) && (i & (1 << B))) a[i] = mulc(a[i], pr, pi);
+        if ((i & (1 << A)) && (i & (1 << B))) cmul_ip(a[i], pr, pi);
 }
 
 template <int M, typename V, typename R>
@@ -212,97 +269,67 @@ __device__ __forceinline__ void g_dk(V (&a)[NR], const double *tab)
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
         const int idx = pext5(i, M);
-        a[i] = mulc(a[i], (R)tab[2 * idx], (R)tab[2 * idx + 1]);
+        cmul_ip(a[i], (R)tab[2 * idx], (R)tab[2 * idx + 1]);
+    }
+}
+
+// One gate record.  C is a compile-time code; the dispatch below is a balanced binary tree of
+// compile-time ranges (7 compare-and-branch levels) instead of the linear compare chain ptxas
+// emits for a 123-way switch.
+template <int C, typename V, typename R>
+__device__ __forceinline__ void gate_case(V (&a)[NR], const double *p, uint64_t lbase, uint32_t ga, uint32_t gb)
+{
+    if constexpr (C < C_U) {
+        g_h<C - C_H>(a);
+    } else if constexpr (C < C_X) {
+        g_u<C - C_U, V, R>(a, p);
+    } else if constexpr (C < C_Y) {
+        g_x<C - C_X>(a);
+    } else if constexpr (C < C_D1) {
+        g_y<C - C_Y>(a);
+    } else if constexpr (C < C_D2) {
+        g_d1<C - C_D1, V, R>(a, (R)p[0], (R)p[1]);
+    } else if constexpr (C < C_CX) {
+        g_d2<C - C_D2, V, R>(a, p);
+    } else if constexpr (C < C_CPH) {
+        constexpr int c = (C - C_CX) / 5, t = (C - C_CX) % 5;
+        if constexpr (c != t) g_cx<c, t>(a);
+    } else if constexpr (C < C_TX) {
+        constexpr int x = (C - C_CPH) / 5, y = (C - C_CPH) % 5;
+        if constexpr (x < y) g_cph<x, y, V, R>(a, (R)p[0], (R)p[1]);
+    } else if constexpr (C < C_TD1) {
+        if ((lbase >> ga) & 1) g_x<C - C_TX>(a);
+    } else if constexpr (C < C_TPH) {
+        if ((lbase >> ga) & 1) g_d1<C - C_TD1, V, R>(a, (R)p[0], (R)p[1]);
+    } else if constexpr (C == C_TPH) {
+        const bool pred = ((lbase >> ga) & 1) && ((lbase >> gb) & 1);
+        const R fr = (R)(pred ? p[2] : p[0]), fi = (R)(pred ? p[3] : p[1]);
+        if (fr != R(1) || fi != R(0)) {
+#pragma unroll
+            for (int i = 0; i < NR; ++i) cmul_ip(a[i], fr, fi);
+        }
+    } else if constexpr (C < C_N) {
+        if constexpr (C - C_DK > 0) g_dk<C - C_DK, V, R>(a, p);
+    }
+}
+
+template <int LO, int HI, typename V, typename R>
+__device__ __forceinline__ void dispatch(int code, V (&a)[NR], const double *p, uint64_t lbase, uint32_t ga,
+                                         uint32_t gb)
+{
+    if constexpr (HI - LO == 1) {
+        gate_case<LO, V, R>(a, p, lbase, ga, gb);
+    } else {
+        constexpr int MID = (LO + HI) / 2;
+        if (code < MID) dispatch<LO, MID, V, R>(code, a, p, lbase, ga, gb);
+        else dispatch<MID, HI, V, R>(code, a, p, lbase, ga, gb);
     }
 }
 
 template <typename V, typename R>
 __device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const double *prm, uint64_t lbase)
 {
-    const double *p = prm + g.pi;
-#define TQ_R5(base, fn)                      \
-    case base + 0: fn<0>; break;             \
-    case base + 1: fn<1>; break;             \
-    case base + 2: fn<2>; break;             \
-    case base + 3: fn<3>; break;             \
-    case base + 4: fn<4>; break;
-#define TQ_CX(c, t) case C_CX + 5 * c + t: g_cx<c, t>(a); break;
-#define TQ_CP(x, y) case C_CPH + 5 * x + y: g_cph<x, y, V, R>(a, (R)p[0], (R)p[1]); break;
-    switch (g.code) {
-    case C_H + 0: g_h<0>(a); break;
-    case C_H + 1: g_h<1>(a); break;
-    case C_H + 2: g_h<2>(a); break;
-    case C_H + 3: g_h<3>(a); break;
-    case C_H + 4: g_h<4>(a); break;
-    case C_U + 0: g_u<0, V, R>(a, p); break;
-    case C_U + 1: g_u<1, V, R>(a, p); break;
-    case C_U + 2: g_u<2, V, R>(a, p); break;
-    case C_U + 3: g_u<3, V, R>(a, p); break;
-    case C_U + 4: g_u<4, V, R>(a, p); break;
-    case C_X + 0: g_x<0>(a); break;
-    case C_X + 1: g_x<1>(a); break;
-    case C_X + 2: g_x<2>(a); break;
-    case C_X + 3: g_x<3>(a); break;
-    case C_X + 4: g_x<4>(a); break;
-    case C_Y + 0: g_y<0>(a); break;
-    case C_Y + 1: g_y<1>(a); break;
-    case C_Y + 2: g_y<2>(a); break;
-    case C_Y + 3: g_y<3>(a); break;
-    case C_Y + 4: g_y<4>(a); break;
-    case C_D1 + 0: g_d1<0, V, R>(a, (R)p[0], (R)p[1]); break;
-    case C_D1 + 1: g_d1<1, V, R>(a, (R)p[0], (R)p[1]); break;
-    case C_D1 + 2: g_d1<2, V, R>(a, (R)p[0], (R)p[1]); break;
-    case C_D1 + 3: g_d1<3, V, R>(a, (R)p[0], (R)p[1]); break;
-    case C_D1 + 4: g_d1<4, V, R>(a, (R)p[0], (R)p[1]); break;
-    case C_D2 + 0: g_d2<0, V, R>(a, p); break;
-    case C_D2 + 1: g_d2<1, V, R>(a, p); break;
-    case C_D2 + 2: g_d2<2, V, R>(a, p); break;
-    case C_D2 + 3: g_d2<3, V, R>(a, p); break;
-    case C_D2 + 4: g_d2<4, V, R>(a, p); break;
-    TQ_CX(0, 1) TQ_CX(0, 2) TQ_CX(0, 3) TQ_CX(0, 4)
-    TQ_CX(1, 0) TQ_CX(1, 2) TQ_CX(1, 3) TQ_CX(1, 4)
-    TQ_CX(2, 0) TQ_CX(2, 1) TQ_CX(2, 3) TQ_CX(2, 4)
-    TQ_CX(3, 0) TQ_CX(3, 1) TQ_CX(3, 2) TQ_CX(3, 4)
-    TQ_CX(4, 0) TQ_CX(4, 1) TQ_CX(4, 2) TQ_CX(4, 3)
-    TQ_CP(0, 1) TQ_CP(0, 2) TQ_CP(0, 3) TQ_CP(0, 4)
-    TQ_CP(1, 2) TQ_CP(1, 3) TQ_CP(1, 4)
-    TQ_CP(2, 3) TQ_CP(2, 4)
-    TQ_CP(3, 4)
-#define TQ_DK(m) case C_DK + m: g_dk<m, V, R>(a, p); break;
-    TQ_DK(1) TQ_DK(2) TQ_DK(3) TQ_DK(4) TQ_DK(5) TQ_DK(6) TQ_DK(7) TQ_DK(8) TQ_DK(9) TQ_DK(10)
-    TQ_DK(11) TQ_DK(12) TQ_DK(13) TQ_DK(14) TQ_DK(15) TQ_DK(16) TQ_DK(17) TQ_DK(18) TQ_DK(19) TQ_DK(20)
-    TQ_DK(21) TQ_DK(22) TQ_DK(23) TQ_DK(24) TQ_DK(25) TQ_DK(26) TQ_DK(27) TQ_DK(28) TQ_DK(29) TQ_DK(30)
-    TQ_DK(31)
-#undef TQ_DK
-    default: {
-        const bool pa = (lbase >> g.a) & 1;
-        if (g.code == C_TPH) {
-            const bool pred = pa && ((lbase >> g.b) & 1);
-            const R fr = (R)(pred ? p[2] : p[0]), fi = (R)(pred ? p[3] : p[1]);
-            if (fr != R(1) || fi != R(0)) {
-#pragma unroll
-                for (int i = 0; i < NR; ++i) a[i] = mulc(a[i], fr, fi);
-            }
-        } else if (pa) {
-            switch (g.code) {
-            case C_TX + 0: g_x<0>(a); break;
-            case C_TX + 1: g_x<1>(a); break;
-            case C_TX + 2: g_x<2>(a); break;
-            case C_TX + 3: g_x<3>(a); break;
-            case C_TX + 4: g_x<4>(a); break;
-            case C_TD1 + 0: g_d1<0, V, R>(a, (R)p[0], (R)p[1]); break;
-            case C_TD1 + 1: g_d1<1, V, R>(a, (R)p[0], (R)p[1]); break;
-            case C_TD1 + 2: g_d1<2, V, R>(a, (R)p[0], (R)p[1]); break;
-            case C_TD1 + 3: g_d1<3, V, R>(a, (R)p[0], (R)p[1]); break;
-            case C_TD1 + 4: g_d1<4, V, R>(a, (R)p[0], (R)p[1]); break;
-            default: break;
-            }
-        }
-    }
-    }
-#undef TQ_R5
-#undef TQ_CX
-#undef TQ_CP
+    dispatch<0, C_N, V, R>(g.code, a, prm + g.pi, lbase, g.a, g.b);
 }
 
 __device__ __forceinline__ uint32_t swz(uint32_t t) { return t ^ ((t >> 3) & 7u); }
@@ -409,7 +436,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 for (int r = 0; r < NR; ++r) { a[r].x *= sr; a[r].y *= sr; }
             } else {
 #pragma unroll
-                for (int r = 0; r < NR; ++r) a[r] = mulc(a[r], sr, si);
+                for (int r = 0; r < NR; ++r) cmul_ip(a[r], sr, si);
             }
         }
         // xm_store has no tile bits: register offsets are additive

@@ -182,6 +182,41 @@ def test_c3_sampled_leaf_slots(T, torch, oracle):
         assert ((got != ref) & ~edge).sum() == 0
 
 
+def test_c4_full_size(T, torch, oracle):
+    # C4 (30 qubits, 16 GiB c128) in bench's launch configuration (fused, hybrid re-anchor):
+    # leaf 0 is the noiseless leaf -> closed form |0x26666664>; rollback over a DFS range equals
+    # a fresh descent; one noisy leaf vs the oracle's full replay (amplitudes and its shot slots).
+    cfg = W.config("C4")
+    t = _cfg_tree(T, cfg)
+    assert t.leaf(0)[0] == []
+    n = cfg.n
+    d = dstate(torch, n, 128)
+    slots, _ = T.run_tree(t, 128, d_state=d, leaf_begin=0, leaf_end=1)
+    idx = W.adder_expected_output(14)
+    assert abs(complex(d[idx].item()) - 1) < 1e-12
+    d[idx] = 0
+    assert float(d.abs().max().item()) < 1e-12
+    assert (slots[:t.leaf(0)[1]] == idx).all()
+    # rollback over the last DFS leaves (errors from gate 25 on, Y/X frozen before T gates)
+    # vs a fresh descent to the last leaf
+    nl = t.n_leaves
+    T.run_tree(t, 128, d_state=d, leaf_begin=nl - 6, leaf_end=nl, flags=T.EXEC_NO_SAMPLE | T.EXEC_NO_RESET)
+    d2 = dstate(torch, n, 128)
+    T.run_tree(t, 128, d_state=d2, leaf_begin=nl - 1, leaf_end=nl, flags=T.EXEC_NO_SAMPLE)
+    torch.cuda.synchronize()
+    assert float((d - d2).abs().max().item()) < 1e-10
+    del d2
+    # that noisy leaf against the oracle (full 2^30 replay on the host)
+    ot = oracle.Tree.from_config(cfg)
+    ref = ot.replay_leaf(nl - 1)
+    got = d.cpu().numpy()
+    assert np.abs(got - ref).max() < 1e-10
+    out = torch.zeros(max(t.leaf(nl - 1)[1], 64), dtype=torch.int64, device="cuda")
+    T.sample(d, n, 128, out.numel(), cfg.seed, nl - 1, out)
+    r, edge = oracle.sample_state(ref, n, cfg.seed, nl - 1, out.numel())
+    assert ((out.cpu().numpy().astype(np.uint64) != r) & ~edge).sum() == 0
+
+
 def test_run_tree_errors(T, torch):
     cfg = W.config("C1")
     t = _cfg_tree(T, cfg)
