@@ -217,12 +217,13 @@ tusq_status tusq_sample(const void *d_state, uint32_t n, uint32_t precision, uin
     uint64_t nb = 1ull << (n - bb);
     double *d_blocks = nullptr;
     uint32_t *d_edges = nullptr;
-    TQ_CUDA(cudaMallocAsync((void **)&d_blocks, (2 * nb + 1) * sizeof(double), st));
+    TQ_CUDA(cudaMallocAsync((void **)&d_blocks, (2 * nb + 16) * sizeof(double), st));
     TQ_CUDA(cudaMallocAsync((void **)&d_edges, sizeof(uint32_t), st));
     TQ_CUDA(cudaMemsetAsync(d_edges, 0, sizeof(uint32_t), st));
     launch_block_sums(d_state, n, (int)precision, bb, d_blocks, st);
     launch_scan_blocks(d_blocks, d_blocks + nb, nb, 0, st);
-    launch_draws(d_state, n, (int)precision, bb, d_blocks + nb, n_draws, seed, leaf, 1e-9, 0, d_out, d_edges, st);
+    launch_draws(d_state, n, (int)precision, bb, d_blocks, d_blocks + nb, n_draws, seed, leaf, 1e-9, 0, d_out,
+                 d_edges, st);
     TQ_CUDA(cudaGetLastError());
     TQ_CUDA(cudaFreeAsync(d_blocks, st));
     TQ_CUDA(cudaFreeAsync(d_edges, st));
@@ -280,7 +281,7 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     } while (0)
     if (!dry) {
         TQ_RUN_CUDA(cudaMalloc((void **)&d_slots, std::max<uint64_t>(1, off1 - off0) * sizeof(uint64_t)));
-        TQ_RUN_CUDA(cudaMalloc((void **)&d_blocks, (2 * nb + 1) * sizeof(double)));
+        TQ_RUN_CUDA(cudaMalloc((void **)&d_blocks, (2 * nb + 16) * sizeof(double)));
         TQ_RUN_CUDA(cudaMalloc((void **)&d_edges, sizeof(uint32_t)));
         TQ_RUN_CUDA(cudaMemsetAsync(d_edges, 0, sizeof(uint32_t), st));
     }
@@ -326,7 +327,9 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
             bool sums = false;
             const bool want_sums = sample && l.count && n >= 12;
             if (fuse) {
-                planner.execute_ex(ops, ctx, reset ? &init : nullptr, want_sums ? d_blocks : nullptr, &sums);
+                // (plan-only runs pass a placeholder pointer: nothing is launched)
+                double *sums_dst = want_sums ? (dry ? reinterpret_cast<double *>(16) : d_blocks) : nullptr;
+                planner.execute_ex(ops, ctx, reset ? &init : nullptr, sums_dst, &sums);
             } else {
                 if (reset) {
                     double b = dry ? (double)need : launch_init_basis(psi, n, prec, init.index, init.re, init.im, st);
@@ -343,8 +346,8 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
                 }
                 if (!dry) {
                     launch_scan_blocks(d_blocks, d_blocks + nb, nb, xm >> bb, st);
-                    stats.sample_bytes += launch_draws(psi, n, prec, bb, d_blocks + nb, l.count, t->seed, li, eps, xm,
-                                                       d_slots + (l.offset - off0), d_edges, st);
+                    stats.sample_bytes += launch_draws(psi, n, prec, bb, d_blocks, d_blocks + nb, l.count, t->seed,
+                                                       li, eps, xm, d_slots + (l.offset - off0), d_edges, st);
                 } else {
                     stats.sample_bytes += (double)l.count * (double)(amp_bytes << bb);
                 }

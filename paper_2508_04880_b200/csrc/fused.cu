@@ -54,7 +54,8 @@ enum Code : uint16_t {
     C_TD1 = 85,   // +r      if pred(q): bit 1 of reg r *= p
     C_TPH = 90,   //         all *= pred(q0)&pred(q1) ? p1 : p0 (4 params)
     C_DK = 91,    // +mask   a[r] *= tab[pext(r, mask)]  (2 * 2^popc(mask) params)
-    C_N = 123
+    C_N = 123,    // number of gate codes
+    C_XPOSE = 123 // transpose registers to phase a
 };
 
 __host__ __device__ constexpr int pext5(int r, int m)
@@ -87,7 +88,7 @@ struct Params {
     double init_re, init_im;
     double scale_re, scale_im;
     uint64_t ntiles;
-    uint32_t flags, nphase;
+    uint32_t flags, nphase, ngate, _pad2;
     uint8_t qs[TB];               // tile-local bit b <-> global qubit qs[b] (ascending)
     uint32_t rx;                  // register bits where xm_load is set: fixed up by X after the load
     uint64_t regm_load;           // global mask of the phase-0 register qubits
@@ -219,13 +220,15 @@ __device__ __forceinline__ void g_x(V (&a)[NR])
 template <int B, typename V>
 __device__ __forceinline__ void g_y(V (&a)[NR])
 {
-    // (Y psi)_0 = -i psi_1, (Y psi)_1 = i psi_0
+    // (Y psi)_0 = -i psi_1, (Y psi)_1 = i psi_0: swap, then in-place (exact) multiplies by -i / +i
+    // (a re/im register exchange here made ptxas copy every amplitude at each gate dispatch)
+    using R = decltype(a[0].x);
 #pragma unroll
     for (int i = 0; i < NR; ++i)
         if (!(i & (1 << B))) {
-            V x = a[i], y = a[i | (1 << B)];
-            a[i].x = y.y; a[i].y = -y.x;
-            a[i | (1 << B)].x = -x.y; a[i | (1 << B)].y = x.x;
+            vswap(a[i], a[i | (1 << B)]);
+            cmul_ip(a[i], R(0), R(-1));
+            cmul_ip(a[i | (1 << B)], R(0), R(1));
         }
 }
 
@@ -391,11 +394,22 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
             }
         }
 
-        for (uint32_t ph = 0; ph < P.nphase; ++ph) {
-            const Phase &cur = P.ph[ph];
-            if (ph > 0) {
-                // transpose registers from the previous layout to this one through shared memory
-                const Phase &prv = P.ph[ph - 1];
+        // ONE flat loop over records; a phase change is just a record (C_XPOSE) so that all paths
+        // join at a single loop header with the amplitudes in one canonical register set (nested
+        // phase/gate loops made ptxas copy every amplitude at each gate iteration).
+        uint32_t ph = 0;
+        uint64_t lbase = base;
+#pragma unroll
+        for (int j = 0; j < 7; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[P.ph[0].tl[j]];
+        for (uint32_t gi = 0; gi < P.ngate; ++gi) {
+            const GRec g = P.g[gi];
+            if (g.code != C_XPOSE) {
+                apply_gate<V, R>(a, g, P.prm, lbase);
+            } else {
+                // transpose registers from the current layout to phase g.a through shared memory
+                const Phase &prv = P.ph[ph];
+                const Phase &cur = P.ph[g.a];
+                ph = g.a;
                 uint32_t tt = 0;
 #pragma unroll
                 for (int j = 0; j < 7; ++j) tt |= ((tid >> j) & 1u) << prv.tl[j];
@@ -416,12 +430,11 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 TQ_LD(16) TQ_LD(17) TQ_LD(18) TQ_LD(19) TQ_LD(20) TQ_LD(21) TQ_LD(22) TQ_LD(23)
                 TQ_LD(24) TQ_LD(25) TQ_LD(26) TQ_LD(27) TQ_LD(28) TQ_LD(29) TQ_LD(30) TQ_LD(31)
 #undef TQ_LD
-            }
-            // logical index bits of this thread (thread + outer bits) for predicates
-            uint64_t lbase = base;
+                // logical index bits of this thread (thread + outer bits) for predicates
+                lbase = base;
 #pragma unroll
-            for (int j = 0; j < 7; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[cur.tl[j]];
-            for (uint32_t gi = cur.g0; gi < cur.g1; ++gi) apply_gate<V, R>(a, P.g[gi], P.prm, lbase);
+                for (int j = 0; j < 7; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[cur.tl[j]];
+            }
         }
 
         // ---- store with the last layout
@@ -897,6 +910,13 @@ static void build_params(const Group &G, uint32_t n, Built &B)
             rs = lookahead(i, regset);
             regset = 0;
             for (uint32_t q : rs) regset |= bit(q);
+            if (!phases.empty()) {
+                GRec x;
+                memset(&x, 0, sizeof(x));
+                x.code = C_XPOSE;
+                x.a = (uint8_t)phases.size();
+                recs.push_back(x);
+            }
             phases.push_back(make_phase(rs, (uint16_t)recs.size()));
         }
         {
@@ -972,7 +992,15 @@ static void build_params(const Group &G, uint32_t n, Built &B)
     if (phases.size() > (size_t)MAXPH || recs.size() > (size_t)MAXG || prm.size() > (size_t)MAXP)
         throw std::runtime_error("fused planner: group exceeds the kernel parameter block");
     P.nphase = (uint32_t)phases.size();
+    P.ngate = (uint32_t)recs.size();
     static const bool dbg = getenv("TUSQ_DEBUG_PLAN") != nullptr;
+    static const bool sigs = getenv("TUSQ_DEBUG_SIGS") != nullptr;
+    if (sigs) {
+        uint64_t h = 1469598103934665603ull;
+        auto mix = [&](uint64_t v) { h ^= v; h *= 1099511628211ull; };
+        for (auto &r : recs) { mix(r.code); if (r.code >= C_TX && r.code <= C_TPH) { mix(r.a); mix(r.b); } }
+        fprintf(stderr, "[sig] %016llx %zu\n", (unsigned long long)h, recs.size());
+    }
     if (dbg) {
         fprintf(stderr, "[plan] ops %zu recs %zu phases %zu prm %zu tile %#llx\n", G.ops.size(), recs.size(),
                 phases.size(), prm.size(), (unsigned long long)tile);
@@ -1025,10 +1053,30 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     // otherwise tile membership for controls/diagonals only while there is room (e.g. QFT)
     static const char *mode_env = getenv("TUSQ_TILE_MODE");
     static const int mode = !mode_env ? 0 : (mode_env[0] == 's' ? 1 : mode_env[0] == 'l' ? 2 : 0);
-    std::vector<Group> groups = make_groups(ops, mode == 1);
+    bool strict = mode == 1;
+    std::vector<Group> groups = make_groups(ops, strict);
     if (mode == 0) {
         std::vector<Group> g2 = make_groups(ops, true);
-        if (g2.size() * 100 <= groups.size() * 105) groups.swap(g2);
+        if (g2.size() * 100 <= groups.size() * 105) { groups.swap(g2); strict = true; }
+    }
+    // The sampler's per-block sums come free from the last sweep if its tile is the contiguous
+    // block {0..11}.  If it is not, try cutting the stream so that the longest suffix touching only
+    // qubits < 12 is its own group -- accepted only when it costs no extra sweep.
+    if (d_sums && !groups.empty()) {
+        size_t s = ops.size();
+        while (s > 0) {
+            const Op &o = ops[s - 1];
+            if (o.q0 >= (uint32_t)TB || (two_qubit(o.kind) && o.q1 >= (uint32_t)TB)) break;
+            --s;
+        }
+        if (s > 0 && s < ops.size()) {
+            std::vector<Op> head(ops.begin(), ops.begin() + s), tail(ops.begin() + s, ops.end());
+            std::vector<Group> g3 = make_groups(head, strict), g4 = make_groups(tail, strict);
+            if (g3.size() + g4.size() <= groups.size()) {
+                g3.insert(g3.end(), g4.begin(), g4.end());
+                groups.swap(g3);
+            }
+        }
     }
     const double s = (double)(1ull << n_) * (prec_ == 128 ? 16 : 8);
     bool pending_init = init != nullptr;

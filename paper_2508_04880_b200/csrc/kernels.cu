@@ -354,8 +354,32 @@ double launch_block_sums(const void *psi, uint32_t n, int prec, uint32_t block_b
     return (double)(1ull << n) * (prec == 64 ? 8.0 : 16.0);
 }
 
-// single-CTA exclusive scan (1024 threads, contiguous chunk per thread).  Input: block sums in
-// PHYSICAL block order; output prefix[b] over LOGICAL blocks b (physical block = b ^ mh).
+// Two-level CDF over blocks: superblocks of SB logical blocks.  k_super sums each superblock
+// (fixed order, deterministic) reading the PHYSICAL block sums (physical block = logical ^ mh);
+// k_scan turns the nsb superblock sums into an exclusive prefix (v[nsb] = total).  A draw then
+// binary-searches superblocks and scans one superblock's block sums with a warp.
+constexpr uint64_t SB = 1024;
+
+__global__ void __launch_bounds__(256) k_super(const double *__restrict__ phys, double *__restrict__ sup, uint64_t nb,
+                                               uint64_t mh)
+{
+    const uint64_t b0 = blockIdx.x * SB;
+    double s = 0.0;
+    for (int j = 0; j < 4; ++j) {
+        const uint64_t i = threadIdx.x * 4 + j;
+        if (b0 + i < nb) s += phys[(b0 + i) ^ mh];
+    }
+    __shared__ double red[8];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        sup[blockIdx.x] = t;
+    }
+}
+
 __global__ void __launch_bounds__(1024) k_scan(const double *__restrict__ phys, double *__restrict__ v, uint64_t nb,
                                                uint64_t mh)
 {
@@ -384,15 +408,20 @@ __global__ void __launch_bounds__(1024) k_scan(const double *__restrict__ phys, 
 
 void launch_scan_blocks(const double *d_phys, double *d_prefix, uint64_t nb, uint64_t mh, cudaStream_t st)
 {
-    k_scan<<<1, 1024, 0, st>>>(d_phys, d_prefix, nb, mh);
+    // d_prefix: nsb superblock sums, then (in place) their exclusive prefix + total
+    const uint64_t nsb = (nb + SB - 1) / SB;
+    double *sup = d_prefix + nsb + 1;   // scratch for the raw superblock sums
+    k_super<<<(unsigned)nsb, 256, 0, st>>>(d_phys, sup, nb, mh);
+    k_scan<<<1, 1024, 0, st>>>(sup, d_prefix, nsb, 0);
 }
 
 // one warp per draw
 template <typename R>
 __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restrict__ psi, uint32_t block_bits,
-                                               const double *__restrict__ prefix, uint64_t nb, uint64_t n_draws,
-                                               uint32_t k0, uint32_t k1, uint64_t leaf, double edge_eps,
-                                               uint64_t xm, uint64_t *__restrict__ out, uint32_t *__restrict__ edges)
+                                               const double *__restrict__ phys, const double *__restrict__ sprefix,
+                                               uint64_t nb, uint64_t n_draws, uint32_t k0, uint32_t k1,
+                                               uint64_t leaf, double edge_eps, uint64_t xm,
+                                               uint64_t *__restrict__ out, uint32_t *__restrict__ edges)
 {
     // logical index i is stored at physical i ^ xm (pending X relabels of the fused path)
     using V = typename CV<R>::T;
@@ -401,15 +430,46 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
     if (warp >= n_draws) return;
     U4 w = philox10(U4{(uint32_t)warp, (uint32_t)leaf, (uint32_t)(leaf >> 32), TAG_SHOT}, k0, k1);
     uint64_t x = (uint64_t)w.x | ((uint64_t)w.y << 32);
-    const double T = prefix[nb];
+    const uint64_t nsb = (nb + SB - 1) / SB;
+    const uint64_t mh = xm >> block_bits;
+    const double T = sprefix[nsb];
     const double t = (double)(x >> 11) * 0x1.0p-53 * T;
-    // first block whose inclusive sum prefix[b+1] exceeds t
-    uint64_t lo = 0, hi = nb - 1;
+    // superblock: first sb whose inclusive prefix sprefix[sb+1] exceeds t
+    uint64_t lo = 0, hi = nsb - 1;
     while (lo < hi) {
         uint64_t mid = (lo + hi) >> 1;
-        if (prefix[mid + 1] > t) hi = mid; else lo = mid + 1;
+        if (sprefix[mid + 1] > t) hi = mid; else lo = mid + 1;
     }
-    const uint64_t b = lo;
+    const uint64_t sb = lo;
+    // block inside the superblock: lane l owns blocks [sb*SB + 32 l, +32)
+    const uint64_t bl0 = sb * SB + 32 * lane;
+    double ls = 0.0;
+    for (uint64_t j = 0; j < 32 && bl0 + j < nb; ++j) ls += phys[(bl0 + j) ^ mh];
+    double lincl = ls;
+    for (int o = 1; o < 32; o <<= 1) {
+        double y = __shfl_up_sync(0xffffffffu, lincl, o);
+        if (lane >= (unsigned)o) lincl += y;
+    }
+    const double sbase = sprefix[sb];
+    unsigned bhit = __ballot_sync(0xffffffffu, sbase + lincl > t);
+    unsigned bl = bhit ? __ffs(bhit) - 1 : 31;
+    while (!bhit && bl > 0 && !__shfl_sync(0xffffffffu, ls > 0.0 ? 1 : 0, bl)) --bl;   // rounding fallback
+    uint64_t b = 0;
+    double bbase = 0.0;
+    if (lane == bl) {
+        double run = sbase + lincl - ls;
+        uint64_t bb = bl0;
+        for (uint64_t j = 0; j < 32 && bl0 + j < nb; ++j) {
+            const double v = phys[(bl0 + j) ^ mh];
+            bb = bl0 + j;
+            if (run + v > t) break;
+            run += v;
+        }
+        b = bb;
+        bbase = run;
+    }
+    b = __shfl_sync(0xffffffffu, b, bl);
+    bbase = __shfl_sync(0xffffffffu, bbase, bl);
     const uint64_t bs = 1ull << block_bits;
     const uint64_t chunk = (bs + 31) / 32;
     const uint64_t c0 = lane * chunk < bs ? lane * chunk : bs, c1 = c0 + chunk < bs ? c0 + chunk : bs;
@@ -431,7 +491,7 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
         double y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= (unsigned)o) incl += y;
     }
-    const double base = prefix[b];
+    const double base = bbase;
     unsigned hit = __ballot_sync(0xffffffffu, base + incl > t);
     uint64_t k = b * bs + bs - 1;
     bool edge = false;
@@ -468,20 +528,20 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
     }
 }
 
-double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_prefix,
-                    uint64_t n_draws, uint64_t seed, uint64_t leaf, double edge_eps, uint64_t xm, uint64_t *d_out,
-                    uint32_t *d_edges, cudaStream_t st)
+double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
+                    const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, double edge_eps,
+                    uint64_t xm, uint64_t *d_out, uint32_t *d_edges, cudaStream_t st)
 {
     if (!n_draws) return 0.0;
     uint64_t nb = 1ull << (n - block_bits);
     unsigned grid = (unsigned)((n_draws * 32 + TPB - 1) / TPB);
     uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
     if (prec == 64)
-        k_draws<float><<<grid, TPB, 0, st>>>((const float2 *)psi, block_bits, d_prefix, nb, n_draws, k0, k1, leaf,
-                                             edge_eps, xm, d_out, d_edges);
+        k_draws<float><<<grid, TPB, 0, st>>>((const float2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0, k1,
+                                             leaf, edge_eps, xm, d_out, d_edges);
     else
-        k_draws<double><<<grid, TPB, 0, st>>>((const double2 *)psi, block_bits, d_prefix, nb, n_draws, k0, k1, leaf,
-                                              edge_eps, xm, d_out, d_edges);
+        k_draws<double><<<grid, TPB, 0, st>>>((const double2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0,
+                                              k1, leaf, edge_eps, xm, d_out, d_edges);
     return (double)n_draws * (double)(1ull << block_bits) * (prec == 64 ? 8.0 : 16.0);
 }
 

@@ -28,13 +28,14 @@ struct SamplerWork {
 // block sums of |amp|^2 over contiguous blocks of 2^block_bits amplitudes
 double launch_block_sums(const void *psi, uint32_t n, int prec, uint32_t block_bits, double *d_blocks,
                          cudaStream_t st);
-// exclusive prefix over LOGICAL blocks of nb block sums given in PHYSICAL order (physical
-// block = logical ^ mh); d_prefix[nb] = total
+// superblock (1024 logical blocks) sums of nb block sums given in PHYSICAL order (physical block =
+// logical ^ mh), then their exclusive prefix: d_prefix[0..nsb] (nsb = ceil(nb/1024)); needs
+// 2*nsb + 2 doubles of d_prefix
 void launch_scan_blocks(const double *d_phys, double *d_prefix, uint64_t nb, uint64_t mh, cudaStream_t st);
 // draws j = 0..n_draws-1 of leaf `leaf` into d_out[j]; logical index i lives at physical i ^ xm
-double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_prefix,
-                    uint64_t n_draws, uint64_t seed, uint64_t leaf, double edge_eps, uint64_t xm, uint64_t *d_out,
-                    uint32_t *d_edges, cudaStream_t st);
+double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
+                    const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, double edge_eps,
+                    uint64_t xm, uint64_t *d_out, uint32_t *d_edges, cudaStream_t st);
 
 int device_sm_count();
 
