@@ -70,7 +70,9 @@ struct Phase {
     uint16_t g0, g1;      // gate range
     uint8_t rl[RB];       // tile-local bit of each register bit
     uint8_t tl[7];        // tile-local bit of each thread bit (lanes 0-4, warps 0-1)
-    uint16_t so[NR];      // tile-local index contribution of register r (host-computed)
+    uint16_t so[NR];      // entering this phase: tile-local index read into register r
+    uint16_t so_out[NR];  // leaving this phase: tile-local index register r is written to
+                          // (they differ when register permutations are absorbed, host-computed)
 };
 
 struct GRec {
@@ -372,26 +374,20 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
             for (int j = 0; j < 7; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[p0.tl[j]];
         }
         if (P.flags & F_INIT) {
-            const uint64_t lt = (base | gthr) ^ P.xm_load;
+            // the same addressing as a load, from a virtual memory holding init at init_index
+            const uint64_t lt = ((base | gthr) ^ P.xm_load) & ~P.regm_load;
 #pragma unroll
             for (int r = 0; r < NR; ++r) {
-                const bool hit = (lt ^ P.gl[r]) == P.init_index;
+                const bool hit = (lt + P.gl[r]) == P.init_index;
                 a[r].x = hit ? (R)P.init_re : R(0);
                 a[r].y = hit ? (R)P.init_im : R(0);
             }
         } else {
-            // physical = logical ^ xm_load; register-position bits of the mask are applied as
-            // in-register X after an additive load
+            // physical = logical ^ xm_load; the mask's register-position bits and any absorbed
+            // leading register permutation are folded into gl[] on the host (additive offsets)
             const V *p0 = psi + (((base | gthr) ^ P.xm_load) & ~P.regm_load);
 #pragma unroll
             for (int r = 0; r < NR; ++r) a[r] = __ldcs(p0 + P.gl[r]);
-            if (P.rx) {
-                if (P.rx & 1) g_x<0>(a);
-                if (P.rx & 2) g_x<1>(a);
-                if (P.rx & 4) g_x<2>(a);
-                if (P.rx & 8) g_x<3>(a);
-                if (P.rx & 16) g_x<4>(a);
-            }
         }
 
         // ONE flat loop over records; a phase change is just a record (C_XPOSE) so that all paths
@@ -414,7 +410,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
 #pragma unroll
                 for (int j = 0; j < 7; ++j) tt |= ((tid >> j) & 1u) << prv.tl[j];
                 __syncthreads();
-#define TQ_ST(r) sm[swz(tt | prv.so[r])] = a[r];
+#define TQ_ST(r) sm[swz(tt | prv.so_out[r])] = a[r];
                 TQ_ST(0) TQ_ST(1) TQ_ST(2) TQ_ST(3) TQ_ST(4) TQ_ST(5) TQ_ST(6) TQ_ST(7)
                 TQ_ST(8) TQ_ST(9) TQ_ST(10) TQ_ST(11) TQ_ST(12) TQ_ST(13) TQ_ST(14) TQ_ST(15)
                 TQ_ST(16) TQ_ST(17) TQ_ST(18) TQ_ST(19) TQ_ST(20) TQ_ST(21) TQ_ST(22) TQ_ST(23)
@@ -711,7 +707,23 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
 struct Built {
     Params P;
     uint64_t tile = 0;
+    uint8_t pin0[NR];      // absorbed entry permutation of phase 0: register r reads pattern pin0[r]
+    uint8_t pout_last[NR]; // absorbed exit permutation of the last phase: register s written as pattern pout[s]
 };
+
+static bool is_perm_rec(uint16_t c)
+{
+    if (c >= C_X && c < C_X + 5) return true;
+    if (c >= C_CX && c < C_CX + 25) return (c - C_CX) / 5 != (c - C_CX) % 5;
+    return false;
+}
+
+static uint32_t perm_apply(uint16_t c, uint32_t r)
+{
+    if (c < C_X + 5) return r ^ (1u << (c - C_X));
+    const uint32_t cb = (c - C_CX) / 5, tb = (c - C_CX) % 5;
+    return ((r >> cb) & 1) ? r ^ (1u << tb) : r;
+}
 
 static void matrix_u(const Op &o, double m[8])
 {
@@ -811,6 +823,7 @@ static void build_params(const Group &G, uint32_t n, Built &B)
             for (int k = 0; k < RB; ++k)
                 if (r & (1 << k)) o |= 1u << ph.rl[k];
             ph.so[r] = (uint16_t)o;
+            ph.so_out[r] = (uint16_t)o;
         }
         return ph;
     };
@@ -989,6 +1002,45 @@ static void build_params(const Group &G, uint32_t n, Built &B)
         phases.push_back(make_phase(rs, 0));
     }
     phases.back().g1 = (uint16_t)recs.size();
+    // Absorb register permutations (in-register X, CX between register bits) at the start of a
+    // phase into its entry offsets and at its end into its exit offsets: a permutation of the 32
+    // registers right after a load/transpose (or before a transpose/store) is free to apply as
+    // a permutation of the addresses it reads/writes.
+    for (int r = 0; r < NR; ++r) { B.pin0[r] = (uint8_t)r; B.pout_last[r] = (uint8_t)r; }
+    {
+        std::vector<GRec> kept;
+        kept.reserve(recs.size());
+        for (size_t p = 0; p < phases.size(); ++p) {
+            Phase &ph = phases[p];
+            size_t g0 = ph.g0, g1 = ph.g1, a = g0, b = g1;
+            while (a < g1 && is_perm_rec(recs[a].code)) ++a;
+            while (b > a && is_perm_rec(recs[b - 1].code)) --b;
+            uint8_t pin[NR], pout[NR];
+            for (uint32_t r = 0; r < (uint32_t)NR; ++r) {
+                uint32_t x = r;                      // a_k[r] = a_0[pi_1(...pi_k(r))]
+                for (size_t j = a; j-- > g0;) x = perm_apply(recs[j].code, x);
+                pin[r] = (uint8_t)x;
+                uint32_t y = r;                      // a_fin[r] = a_m[pi_b(...pi_end(r))]
+                for (size_t j = g1; j-- > b;) y = perm_apply(recs[j].code, y);
+                pout[r] = (uint8_t)y;
+            }
+            uint16_t base_so[NR];
+            memcpy(base_so, ph.so, sizeof(base_so));
+            for (int r = 0; r < NR; ++r) {
+                ph.so[r] = base_so[pin[r]];          // register r reads the pattern pin[r]
+                ph.so_out[pout[r]] = base_so[r];     // register pout[r] holds the value of pattern r
+            }
+            if (p == 0) memcpy(B.pin0, pin, sizeof(pin));
+            if (p + 1 == phases.size())
+                for (int r = 0; r < NR; ++r) B.pout_last[pout[r]] = (uint8_t)r;
+            if (p > 0) kept.push_back(recs[g0 - 1]);   // the XPOSE record entering this phase
+            const uint16_t ng0 = (uint16_t)kept.size();
+            for (size_t j = a; j < b; ++j) kept.push_back(recs[j]);
+            ph.g0 = ng0;
+            ph.g1 = (uint16_t)kept.size();
+        }
+        recs.swap(kept);
+    }
     if (phases.size() > (size_t)MAXPH || recs.size() > (size_t)MAXG || prm.size() > (size_t)MAXP)
         throw std::runtime_error("fused planner: group exceeds the kernel parameter block");
     P.nphase = (uint32_t)phases.size();
@@ -1106,13 +1158,19 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 P.regm_load |= bit(P.qs[f.rl[k]]);
                 if (m_load & bit(P.qs[f.rl[k]])) P.rx |= 1u << k;
             }
-            for (int r = 0; r < NR; ++r) {
-                uint64_t a = 0, b = 0;
+            auto goff = [&](const Phase &ph, uint32_t pat) {
+                uint64_t o = 0;
                 for (int k = 0; k < RB; ++k)
-                    if (r & (1 << k)) { a |= bit(P.qs[f.rl[k]]); b |= bit(P.qs[l.rl[k]]); }
-                P.gl[r] = a;
-                P.gs[r] = b;
+                    if (pat & (1u << k)) o |= bit(P.qs[ph.rl[k]]);
+                return o;
+            };
+            // register r loads physical pattern pin0[r] ^ rx (mask fix-up + absorbed permutation);
+            // register s is stored at the pattern pout_last[s]
+            for (int r = 0; r < NR; ++r) {
+                P.gl[r] = goff(f, (uint32_t)B.pin0[r] ^ P.rx);
+                P.gs[r] = goff(l, B.pout_last[r]);
             }
+            P.rx = 0;
         }
         P.ntiles = 1ull << (n_ - TB);
         P.flags = 0;
