@@ -337,7 +337,10 @@ __device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const doub
     dispatch<0, C_N, V, R>(g.code, a, prm + g.pi, lbase, g.a, g.b);
 }
 
-__device__ __forceinline__ uint32_t swz(uint32_t t) { return t ^ ((t >> 3) & 7u); }
+// shared-memory swizzle of a 12-bit tile index: the 16-byte slot's low 3 bits (its bank group
+// within a 128-byte wavefront) XOR a fold of the 9 high bits, so that the 8 lanes of a
+// quarter-warp hit distinct bank groups whichever 3 tile bits the lanes carry in a phase layout
+__device__ __forceinline__ uint32_t swz(uint32_t t) { return t ^ (((t >> 3) ^ (t >> 6) ^ (t >> 9)) & 7u); }
 
 template <int R_>
 __device__ __forceinline__ uint32_t roff32(const uint32_t (&rb)[RB])
