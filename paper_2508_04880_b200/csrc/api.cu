@@ -297,6 +297,7 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     std::vector<Op> ops;
     ops.reserve(4 * t->gates.size() + 64);
     uint64_t since_anchor = 0;
+    bool phys_sums_valid = false;
     try {
         for (uint64_t li = lb; li < le; ++li) {
             const Leaf &l = t->leaves[li];
@@ -324,6 +325,7 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
                 since_anchor = ops.size();
             }
             stats.gate_apps += ops.size();
+            const uint64_t sweeps_before = stats.sweeps;
             bool sums = false;
             const bool want_sums = sample && l.count && n >= 12;
             if (fuse) {
@@ -338,11 +340,16 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
                 }
                 execute_unfused(ops, ctx);
             }
+            // per-block |amp|^2 sums are PHYSICAL-block sums: still valid after a transition that only
+            // relabelled (pending X mask), recomputed when the state changed without an epilogue
+            if (sums) phys_sums_valid = true;
+            else if (reset || stats.sweeps != sweeps_before) phys_sums_valid = false;
             if (sample && l.count) {
                 const uint64_t xm = fuse ? planner.xmask() : 0;
-                if (!sums) {
+                if (!phys_sums_valid) {
                     stats.sample_bytes += dry ? (double)need : launch_block_sums(psi, n, prec, bb, d_blocks, st);
                     stats.launches++;
+                    phys_sums_valid = true;
                 }
                 if (!dry) {
                     launch_scan_blocks(d_blocks, d_blocks + nb, nb, xm >> bb, st);

@@ -34,9 +34,13 @@ namespace tq {
 namespace fk {
 
 constexpr int TB = 12;     // tile bits
-constexpr int RB = 5;      // register bits
-constexpr int NR = 32;     // amplitudes per thread
-constexpr int NT = 128;    // threads per CTA
+#ifndef TQ_RB
+#define TQ_RB 5
+#endif
+constexpr int RB = TQ_RB;          // register bits (5: 32 amplitudes per thread, 4: 16)
+constexpr int NR = 1 << RB;        // amplitudes per thread
+constexpr int NTB = TB - RB;       // thread bits (5 lane bits + warp bits)
+constexpr int NT = 1 << NTB;       // threads per CTA
 constexpr int MAXPH = 24;
 constexpr int MAXG = 400;
 constexpr int MAXP = 1600;
@@ -69,7 +73,7 @@ __host__ __device__ constexpr int pext5(int r, int m)
 struct Phase {
     uint16_t g0, g1;      // gate range
     uint8_t rl[RB];       // tile-local bit of each register bit
-    uint8_t tl[7];        // tile-local bit of each thread bit (lanes 0-4, warps 0-1)
+    uint8_t tl[8];        // tile-local bit of each thread bit (lanes 0-4, then warp bits)
     uint16_t so[NR];      // entering this phase: tile-local index read into register r
     uint16_t so_out[NR];  // leaving this phase: tile-local index register r is written to
                           // (they differ when register permutations are absorbed, host-computed)
@@ -271,20 +275,40 @@ __device__ __forceinline__ void g_cph(V (&a)[NR], R pr, R pi)
 template <int M, typename V, typename R>
 __device__ __forceinline__ void g_dk(V (&a)[NR], const double *tab)
 {
+    // one warp-uniform branch per table entry: entries equal to 1 (about half of a Toffoli core's
+    // phase table) cost nothing
+    constexpr int K = __builtin_popcount(M);
 #pragma unroll
-    for (int i = 0; i < NR; ++i) {
-        const int idx = pext5(i, M);
-        cmul_ip(a[i], (R)tab[2 * idx], (R)tab[2 * idx + 1]);
+    for (int idx = 0; idx < (1 << K); ++idx) {
+        const R pr = (R)tab[2 * idx], pi = (R)tab[2 * idx + 1];
+        if (pr != R(1) || pi != R(0)) {
+#pragma unroll
+            for (int i = 0; i < NR; ++i)
+                if (pext5(i, M) == idx) cmul_ip(a[i], pr, pi);
+        }
     }
 }
 
 // One gate record.  C is a compile-time code; the dispatch below is a balanced binary tree of
 // compile-time ranges (7 compare-and-branch levels) instead of the linear compare chain ptxas
 // emits for a 123-way switch.
+// does code C only name register positions < RB (and DK masks < NR)?
+__host__ __device__ constexpr bool code_ok(int C)
+{
+    if (C < C_CX) return (C % 5) < RB;
+    if (C < C_CPH) return (C - C_CX) / 5 < RB && (C - C_CX) % 5 < RB;
+    if (C < C_TX) return (C - C_CPH) / 5 < RB && (C - C_CPH) % 5 < RB;
+    if (C < C_TPH) return (C - C_TX) % 5 < RB;
+    if (C == C_TPH) return true;
+    return C - C_DK < NR;
+}
+
 template <int C, typename V, typename R>
 __device__ __forceinline__ void gate_case(V (&a)[NR], const double *p, uint64_t lbase, uint32_t ga, uint32_t gb)
 {
-    if constexpr (C < C_U) {
+    if constexpr (!code_ok(C)) {
+        return;
+    } else if constexpr (C < C_U) {
         g_h<C - C_H>(a);
     } else if constexpr (C < C_X) {
         g_u<C - C_U, V, R>(a, p);
@@ -374,7 +398,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
         {
             const Phase &p0 = P.ph[0];
 #pragma unroll
-            for (int j = 0; j < 7; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[p0.tl[j]];
+            for (int j = 0; j < NTB; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[p0.tl[j]];
         }
         if (P.flags & F_INIT) {
             // the same addressing as a load, from a virtual memory holding init at init_index
@@ -399,7 +423,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
         uint32_t ph = 0;
         uint64_t lbase = base;
 #pragma unroll
-        for (int j = 0; j < 7; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[P.ph[0].tl[j]];
+        for (int j = 0; j < NTB; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[P.ph[0].tl[j]];
         for (uint32_t gi = 0; gi < P.ngate; ++gi) {
             const GRec g = P.g[gi];
             if (g.code != C_XPOSE) {
@@ -411,9 +435,9 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 ph = g.a;
                 uint32_t tt = 0;
 #pragma unroll
-                for (int j = 0; j < 7; ++j) tt |= ((tid >> j) & 1u) << prv.tl[j];
+                for (int j = 0; j < NTB; ++j) tt |= ((tid >> j) & 1u) << prv.tl[j];
                 __syncthreads();
-#define TQ_ST(r) sm[swz(tt | prv.so_out[r])] = a[r];
+#define TQ_ST(r) if constexpr (r < NR) sm[swz(tt | prv.so_out[r])] = a[r];
                 TQ_ST(0) TQ_ST(1) TQ_ST(2) TQ_ST(3) TQ_ST(4) TQ_ST(5) TQ_ST(6) TQ_ST(7)
                 TQ_ST(8) TQ_ST(9) TQ_ST(10) TQ_ST(11) TQ_ST(12) TQ_ST(13) TQ_ST(14) TQ_ST(15)
                 TQ_ST(16) TQ_ST(17) TQ_ST(18) TQ_ST(19) TQ_ST(20) TQ_ST(21) TQ_ST(22) TQ_ST(23)
@@ -422,8 +446,8 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 __syncthreads();
                 tt = 0;
 #pragma unroll
-                for (int j = 0; j < 7; ++j) tt |= ((tid >> j) & 1u) << cur.tl[j];
-#define TQ_LD(r) a[r] = sm[swz(tt | cur.so[r])];
+                for (int j = 0; j < NTB; ++j) tt |= ((tid >> j) & 1u) << cur.tl[j];
+#define TQ_LD(r) if constexpr (r < NR) a[r] = sm[swz(tt | cur.so[r])];
                 TQ_LD(0) TQ_LD(1) TQ_LD(2) TQ_LD(3) TQ_LD(4) TQ_LD(5) TQ_LD(6) TQ_LD(7)
                 TQ_LD(8) TQ_LD(9) TQ_LD(10) TQ_LD(11) TQ_LD(12) TQ_LD(13) TQ_LD(14) TQ_LD(15)
                 TQ_LD(16) TQ_LD(17) TQ_LD(18) TQ_LD(19) TQ_LD(20) TQ_LD(21) TQ_LD(22) TQ_LD(23)
@@ -432,7 +456,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 // logical index bits of this thread (thread + outer bits) for predicates
                 lbase = base;
 #pragma unroll
-                for (int j = 0; j < 7; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[cur.tl[j]];
+                for (int j = 0; j < NTB; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[cur.tl[j]];
             }
         }
 
@@ -440,7 +464,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
         const Phase &last = P.ph[P.nphase - 1];
         gthr = 0;
 #pragma unroll
-        for (int j = 0; j < 7; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[last.tl[j]];
+        for (int j = 0; j < NTB; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[last.tl[j]];
         if (P.flags & F_SCALE) {
             const R sr = (R)P.scale_re, si = (R)P.scale_im;
             if (si == R(0)) {
@@ -466,7 +490,12 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
             for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
             if ((tid & 31) == 0) red[tid >> 5] = s;
             __syncthreads();
-            if (tid == 0) sums[(base ^ P.xm_store) >> TB] = red[0] + red[1] + red[2] + red[3];
+            if (tid == 0) {
+                double t = 0.0;
+#pragma unroll
+                for (int w = 0; w < NT / 32; ++w) t += red[w];
+                sums[(base ^ P.xm_store) >> TB] = t;
+            }
             __syncthreads();
         }
     }
@@ -768,12 +797,22 @@ static void build_params(const Group &G, uint32_t n, Built &B)
             if (tile & bit(q)) { P.qs[b] = (uint8_t)q; loc[q] = (uint8_t)b; ++b; }
     }
     // register-need sequence
-    std::vector<int> needq(G.ops.size(), -1);
+    // needq: the qubit an op must have in a register (exchange target); ctrlq: a CX control that
+    // also triggers a phase switch when it is a tile qubit outside the registers -- a register
+    // control turns a whole-register predicated X (TX) into half the swaps and lets Toffoli
+    // cores fold into one diagonal table (measured: ~2.5 TX records per Adder group otherwise)
+    std::vector<int> needq(G.ops.size(), -1), ctrlq(G.ops.size(), -1);
     for (size_t i = 0; i < G.ops.size(); ++i) {
         const Op &o = G.ops[i].op;
         if (is_exchange(o) || G.ops[i].in_tile_xy) needq[i] = (int)o.q0;
-        else if (o.kind == CX) needq[i] = (int)o.q1;
+        else if (o.kind == CX) {
+            needq[i] = (int)o.q1;
+            if (tile & bit(o.q0)) ctrlq[i] = (int)o.q0;
+        }
     }
+    auto needs_switch = [&](size_t i, uint64_t regs) {
+        return (needq[i] >= 0 && !(regs & bit(needq[i]))) || (ctrlq[i] >= 0 && !(regs & bit(ctrlq[i])));
+    };
     auto lookahead = [&](size_t from, uint64_t keep) {
         std::vector<uint32_t> rs;
         uint64_t have = 0;
@@ -819,7 +858,7 @@ static void build_params(const Group &G, uint32_t n, Built &B)
             used |= 1u << pick;
             ph.tl[tj++] = (uint8_t)pick;
         }
-        for (uint32_t b = 0; b < (uint32_t)TB && tj < 7; ++b)
+        for (uint32_t b = 0; b < (uint32_t)TB && tj < NTB; ++b)
             if (!(used & (1u << b))) { used |= 1u << b; ph.tl[tj++] = (uint8_t)b; }
         for (int r = 0; r < NR; ++r) {
             uint32_t o = 0;
@@ -868,7 +907,7 @@ static void build_params(const Group &G, uint32_t n, Built &B)
         uint32_t best_mask = 0;
         double br[NR], bi[NR];
         for (size_t j = i; j < G.ops.size() && classical(j); ++j) {
-            if (needq[j] >= 0 && !(regset & bit(needq[j]))) break;
+            if (needs_switch(j, regset)) break;
             const Op &o = G.ops[j].op;
             const int a = regpos(o.q0), b = two_qubit(o.kind) ? regpos(o.q1) : -1;
             mask |= 1u << a;
@@ -921,7 +960,7 @@ static void build_params(const Group &G, uint32_t n, Built &B)
     };
     std::vector<double> ftab;
     for (size_t i = 0; i < G.ops.size(); ++i) {
-        if (phases.empty() || (needq[i] >= 0 && !(regset & bit(needq[i])))) {
+        if (phases.empty() || needs_switch(i, regset)) {
             if (!phases.empty()) phases.back().g1 = (uint16_t)recs.size();
             rs = lookahead(i, regset);
             regset = 0;
