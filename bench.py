@@ -196,7 +196,7 @@ def main():
     state = torch.empty(1 << n, dtype=dt, device="cuda")
     stream = torch.cuda.current_stream()
     nleaf = max(le - lb, 1)
-    B = args.leaves_per_step or max(1, min(nleaf, 16 if n >= 28 else 256))
+    B = args.leaves_per_step or max(1, min(nleaf, 64 if n >= 28 else 256))
     slots = np.zeros(cfg.shots, dtype=np.uint64)
 
     # consecutive batches of the rank's DFS range; each step continues the traversal where the

@@ -781,7 +781,7 @@ static bool diag_of(const Op &o, double d[4])
     }
 }
 
-static void build_params(const Group &G, uint32_t n, Built &B)
+static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
 {
     Params &P = B.P;
     memset(&P, 0, sizeof(P));
@@ -1044,6 +1044,45 @@ static void build_params(const Group &G, uint32_t n, Built &B)
         phases.push_back(make_phase(rs, 0));
     }
     phases.back().g1 = (uint16_t)recs.size();
+    // Coalescing: global loads/stores want lanes 0-2 on tile bits 0-2 (qubits 0,1,2: 128-byte
+    // runs).  If the first (last) phase keeps one of those in a register, load (store) through an
+    // extra layout phase and one shared-memory transpose instead (measured: 32 sectors per request,
+    // 2x L2 over-fetch and LSU throttling otherwise).
+    {
+        auto low_in_regs = [&](const Phase &ph) {
+            for (int k = 0; k < RB; ++k)
+                if (ph.rl[k] < 3) return true;
+            return false;
+        };
+        auto canonical = [&]() {
+            std::vector<uint32_t> c;
+            for (uint32_t b = 3; b < (uint32_t)TB && c.size() < (size_t)RB; ++b) c.push_back(P.qs[b]);
+            return c;
+        };
+        if (will_load && low_in_regs(phases.front())) {
+            Phase c = make_phase(canonical(), 0);
+            c.g1 = 0;
+            for (auto &r : recs)
+                if (r.code == C_XPOSE) r.a++;
+            for (auto &ph : phases) { ph.g0++; ph.g1++; }
+            GRec x;
+            memset(&x, 0, sizeof(x));
+            x.code = C_XPOSE;
+            x.a = 1;
+            recs.insert(recs.begin(), x);
+            phases.insert(phases.begin(), c);
+        }
+        if (low_in_regs(phases.back())) {
+            GRec x;
+            memset(&x, 0, sizeof(x));
+            x.code = C_XPOSE;
+            x.a = (uint8_t)phases.size();
+            recs.push_back(x);
+            Phase c = make_phase(canonical(), (uint16_t)recs.size());
+            c.g1 = (uint16_t)recs.size();
+            phases.push_back(c);
+        }
+    }
     // Absorb register permutations (in-register X, CX between register bits) at the start of a
     // phase into its entry offsets and at its end into its exit offsets: a permutation of the 32
     // registers right after a load/transpose (or before a transpose/store) is free to apply as
@@ -1187,7 +1226,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             xmask_ ^= G.xb ^ G.xa;
             continue;
         }
-        build_params(G, n_, B);
+        build_params(G, n_, B, !pending_init);
         Params &P = B.P;
         uint64_t m_load = (pending_init ? 0 : xmask_) ^ G.xb;
         P.xm_load = m_load;
