@@ -96,8 +96,11 @@ struct Params {
     uint64_t ntiles;
     uint32_t flags, nphase, ngate, _pad2;
     uint8_t qs[TB];               // tile-local bit b <-> global qubit qs[b] (ascending)
-    uint32_t rx;                  // register bits where xm_load is set: fixed up by X after the load
+    uint32_t rx;                  // register bits where xm_load is set (folded into gl, kept 0)
+    uint16_t mloc;                // tile-local bits of xm_load (applied when copying to shared memory)
+    uint16_t last_xpose;          // record index of the last transpose (0xFFFF: none)
     uint64_t regm_load;           // global mask of the phase-0 register qubits
+    uint64_t gj[NR];              // global offset of tile-local index (j << NTB) (copy slots)
     uint64_t gl[NR];              // phase 0: global element offset of register r (additive)
     uint64_t gs[NR];              // last phase: global element offset of register r (additive)
     Phase ph[MAXPH];
@@ -376,6 +379,39 @@ __device__ __forceinline__ uint32_t roff32(const uint32_t (&rb)[RB])
     return o;
 }
 
+// asynchronous global -> shared copies (LDGSTS): the next tile streams into shared memory while the
+// current one computes
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    if constexpr (BYTES == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t tile_base(uint64_t T, const uint8_t (&qs)[TB])
+{
+    uint64_t base = T;
+#pragma unroll
+    for (int b = 0; b < TB; ++b) base = ins0(base, qs[b]);
+    return base;
+}
+
+// Copy tile T (physical tile base = logical base ^ xm_store) into shared memory in LOGICAL
+// tile order: thread tid copies physical local indices p = tid + NT*j (coalesced: lanes 0-7 run
+// over qubits 0,1,2), to slot swz(p ^ mloc).
+template <typename V>
+__device__ __forceinline__ void prefetch_tile(V *sm, const V *psi, uint64_t T, const Params &P, uint64_t gt,
+                                              uint32_t tid)
+{
+    const V *src = psi + (tile_base(T, P.qs) ^ P.xm_store) + gt;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) cp_async<sizeof(V)>(sm + swz((tid + (uint32_t)NT * j) ^ P.mloc), src + P.gj[j]);
+    cp_async_commit();
+}
+
 template <typename R>
 __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ psi, const __grid_constant__ Params P,
                                              double *__restrict__ sums)
@@ -385,12 +421,17 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
     V *sm = reinterpret_cast<V *>(smraw);
     __shared__ double red[NT / 32];
     const uint32_t tid = threadIdx.x;
+    const bool init = P.flags & F_INIT;
+    // global offset of this thread's copy slot: tile-local bits 0..NTB-1 = tid (tile independent)
+    uint64_t gt = 0;
+#pragma unroll
+    for (int b = 0; b < NTB; ++b) gt |= (uint64_t)((tid >> b) & 1u) << P.qs[b];
+    if (!init && blockIdx.x < P.ntiles) prefetch_tile(sm, psi, blockIdx.x, P, gt, tid);
     V a[NR];
     for (uint64_t T = blockIdx.x; T < P.ntiles; T += gridDim.x) {
         // logical tile base: the tile index deposited into the outer (non-tile) qubit positions
-        uint64_t base = T;
-#pragma unroll
-        for (int b = 0; b < TB; ++b) base = ins0(base, P.qs[b]);
+        const uint64_t base = tile_base(T, P.qs);
+        const uint64_t Tn = T + gridDim.x;
 
         // ---- phase 0 layout: global offset of this thread's bits; register offsets come from
         // the parameter block (constant bank), added to one base pointer
@@ -400,7 +441,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
 #pragma unroll
             for (int j = 0; j < NTB; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[p0.tl[j]];
         }
-        if (P.flags & F_INIT) {
+        if (init) {
             // the same addressing as a load, from a virtual memory holding init at init_index
             const uint64_t lt = ((base | gthr) ^ P.xm_load) & ~P.regm_load;
 #pragma unroll
@@ -410,11 +451,18 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 a[r].y = hit ? (R)P.init_im : R(0);
             }
         } else {
-            // physical = logical ^ xm_load; the mask's register-position bits and any absorbed
-            // leading register permutation are folded into gl[] on the host (additive offsets)
-            const V *p0 = psi + (((base | gthr) ^ P.xm_load) & ~P.regm_load);
+            // the tile has landed in shared memory in logical order: read it in the phase-0 layout
+            cp_async_wait_all();
+            __syncthreads();
+            uint32_t t0 = 0;
 #pragma unroll
-            for (int r = 0; r < NR; ++r) a[r] = __ldcs(p0 + P.gl[r]);
+            for (int j = 0; j < NTB; ++j) t0 |= ((tid >> j) & 1u) << P.ph[0].tl[j];
+#pragma unroll
+            for (int r = 0; r < NR; ++r) a[r] = sm[swz(t0 | P.ph[0].so[r])];
+            if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: prefetch right away
+                __syncthreads();
+                if (Tn < P.ntiles) prefetch_tile(sm, psi, Tn, P, gt, tid);
+            }
         }
 
         // ONE flat loop over records; a phase change is just a record (C_XPOSE) so that all paths
@@ -457,6 +505,10 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 lbase = base;
 #pragma unroll
                 for (int j = 0; j < NTB; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[cur.tl[j]];
+                if (gi == P.last_xpose && !init) {   // shared memory is free until the next tile
+                    __syncthreads();
+                    if (Tn < P.ntiles) prefetch_tile(sm, psi, Tn, P, gt, tid);
+                }
             }
         }
 
@@ -1226,7 +1278,8 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             xmask_ ^= G.xb ^ G.xa;
             continue;
         }
-        build_params(G, n_, B, !pending_init);
+        // loads go through shared memory (always coalesced): no load-layout phase needed
+        build_params(G, n_, B, false);
         Params &P = B.P;
         uint64_t m_load = (pending_init ? 0 : xmask_) ^ G.xb;
         P.xm_load = m_load;
@@ -1252,6 +1305,19 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 P.gs[r] = goff(l, B.pout_last[r]);
             }
             P.rx = 0;
+            // shared-memory staging of loads: copy-slot offsets, tile-local XOR mask, last transpose
+            P.mloc = 0;
+            for (int b = 0; b < TB; ++b)
+                if (m_load & bit(P.qs[b])) P.mloc |= (uint16_t)(1u << b);
+            for (int j = 0; j < NR; ++j) {
+                uint64_t o = 0;
+                for (int k = 0; k < RB; ++k)
+                    if (j & (1 << k)) o |= bit(P.qs[NTB + k]);
+                P.gj[j] = o;
+            }
+            P.last_xpose = 0xFFFFu;
+            for (uint32_t i = 0; i < P.ngate; ++i)
+                if (P.g[i].code == C_XPOSE) P.last_xpose = (uint16_t)i;
         }
         P.ntiles = 1ull << (n_ - TB);
         P.flags = 0;
