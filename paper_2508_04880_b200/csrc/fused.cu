@@ -950,13 +950,14 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         if (diag_of(o, d)) return inreg(o.q0);
         return false;
     };
-    auto try_fold = [&](size_t i, size_t &fe, uint32_t &fmask, std::vector<double> &tab) -> bool {
+    // net permutation x -> x ^ c (an X translation, c may be 0) folds into the table followed by X's
+    auto try_fold = [&](size_t i, size_t &fe, uint32_t &fmask, std::vector<double> &tab, uint32_t &fxor) -> bool {
         uint8_t perm[NR];
         double pr[NR], pi[NR];
         for (int x = 0; x < NR; ++x) { perm[x] = (uint8_t)x; pr[x] = 1.0; pi[x] = 0.0; }
         uint32_t mask = 0;
         size_t best = i;
-        uint32_t best_mask = 0;
+        uint32_t best_mask = 0, best_xor = 0;
         double br[NR], bi[NR];
         for (size_t j = i; j < G.ops.size() && classical(j); ++j) {
             if (needs_switch(j, regset)) break;
@@ -986,11 +987,14 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                 pr[x] = nr; pi[x] = ni;
                 perm[x] = (uint8_t)y;
             }
-            bool ident = true;
-            for (int x = 0; x < NR && ident; ++x) ident = perm[x] == x;
-            if (ident) {
+            const uint32_t c = perm[0];
+            bool xlat = true;
+            for (int x = 0; x < NR && xlat; ++x) xlat = (uint32_t)perm[x] == ((uint32_t)x ^ c);
+            // a translation costs one X record per set bit of c; require the fold to pay for them
+            if (xlat && (j + 1) - i >= 2 + (size_t)__builtin_popcount(c)) {
                 best = j + 1;
                 best_mask = mask;
+                best_xor = c;
                 memcpy(br, pr, sizeof(br));
                 memcpy(bi, pi, sizeof(bi));
             }
@@ -998,6 +1002,7 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         if (best < i + 2) return false;
         fe = best;
         fmask = best_mask;
+        fxor = best_xor;
         tab.clear();
         const int k = __builtin_popcount(fmask);
         for (int idx = 0; idx < (1 << k); ++idx) {
@@ -1028,14 +1033,22 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         }
         {
             size_t fe = i;
-            uint32_t fmask = 0;
-            if (try_fold(i, fe, fmask, ftab)) {
+            uint32_t fmask = 0, fxor = 0;
+            if (try_fold(i, fe, fmask, ftab, fxor)) {
+                // M|x> = ph(x) |x ^ c>: diagonal table on the input pattern, then X on the bits of c
                 GRec r;
                 memset(&r, 0, sizeof(r));
                 r.code = C_DK + fmask;
                 r.pi = (uint16_t)prm.size();
                 prm.insert(prm.end(), ftab.begin(), ftab.end());
                 recs.push_back(r);
+                for (int b = 0; b < RB; ++b)
+                    if (fxor & (1u << b)) {
+                        GRec xr;
+                        memset(&xr, 0, sizeof(xr));
+                        xr.code = C_X + b;
+                        recs.push_back(xr);
+                    }
                 i = fe - 1;
                 continue;
             }
