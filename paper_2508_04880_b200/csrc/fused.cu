@@ -58,8 +58,9 @@ enum Code : uint16_t {
     C_TD1 = 85,   // +r      if pred(q): bit 1 of reg r *= p
     C_TPH = 90,   //         all *= pred(q0)&pred(q1) ? p1 : p0 (4 params)
     C_DK = 91,    // +mask   a[r] *= tab[pext(r, mask)]  (2 * 2^popc(mask) params)
-    C_N = 123,    // number of gate codes
-    C_XPOSE = 123 // transpose registers to phase a
+    C_CX2 = 123,  // +25c+5t1+t2 (t1 < t2): CX(c->t1) CX(c->t2) as ONE swap pass
+    C_N = 248,    // number of gate codes
+    C_XPOSE = 248 // transpose registers to phase a
 };
 
 __host__ __device__ constexpr int pext5(int r, int m)
@@ -259,6 +260,15 @@ __device__ __forceinline__ void g_d2(V (&a)[NR], const double *p)
     }
 }
 
+// CX(c->t1) then CX(c->t2): control-1 registers r move to r ^ t1 ^ t2 -- 8 swaps, like one CX
+template <int C, int T1, int T2, typename V>
+__device__ __forceinline__ void g_cx2(V (&a)[NR])
+{
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+        if ((i & (1 << C)) && !(i & (1 << T1))) vswap(a[i], a[i ^ (1 << T1) ^ (1 << T2)]);
+}
+
 template <int C, int T, typename V>
 __device__ __forceinline__ void g_cx(V (&a)[NR])
 {
@@ -303,7 +313,9 @@ __host__ __device__ constexpr bool code_ok(int C)
     if (C < C_TX) return (C - C_CPH) / 5 < RB && (C - C_CPH) % 5 < RB;
     if (C < C_TPH) return (C - C_TX) % 5 < RB;
     if (C == C_TPH) return true;
-    return C - C_DK < NR;
+    if (C < C_CX2) return C - C_DK < NR;
+    const int c = (C - C_CX2) / 25, t1 = (C - C_CX2) / 5 % 5, t2 = (C - C_CX2) % 5;
+    return c < RB && t1 < RB && t2 < RB && t1 < t2 && c != t1 && c != t2;
 }
 
 template <int C, typename V, typename R>
@@ -340,6 +352,9 @@ __device__ __forceinline__ void gate_case(V (&a)[NR], const double *p, uint64_t 
 #pragma unroll
             for (int i = 0; i < NR; ++i) cmul_ip(a[i], fr, fi);
         }
+    } else if constexpr (C >= C_CX2) {
+        constexpr int c = (C - C_CX2) / 25, t1 = (C - C_CX2) / 5 % 5, t2 = (C - C_CX2) % 5;
+        g_cx2<c, t1, t2>(a);
     } else if constexpr (C < C_N) {
         if constexpr (C - C_DK > 0) g_dk<C - C_DK, V, R>(a, p);
     }
@@ -799,12 +814,17 @@ static bool is_perm_rec(uint16_t c)
 {
     if (c >= C_X && c < C_X + 5) return true;
     if (c >= C_CX && c < C_CX + 25) return (c - C_CX) / 5 != (c - C_CX) % 5;
+    if (c >= C_CX2 && c < C_N) return code_ok(c);
     return false;
 }
 
 static uint32_t perm_apply(uint16_t c, uint32_t r)
 {
     if (c < C_X + 5) return r ^ (1u << (c - C_X));
+    if (c >= C_CX2) {
+        const uint32_t cb = (c - C_CX2) / 25, t1 = (c - C_CX2) / 5 % 5, t2 = (c - C_CX2) % 5;
+        return ((r >> cb) & 1) ? r ^ (1u << t1) ^ (1u << t2) : r;
+    }
     const uint32_t cb = (c - C_CX) / 5, tb = (c - C_CX) % 5;
     return ((r >> cb) & 1) ? r ^ (1u << tb) : r;
 }
@@ -1109,6 +1129,34 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         phases.push_back(make_phase(rs, 0));
     }
     phases.back().g1 = (uint16_t)recs.size();
+    // Merge adjacent CX records sharing a control (the two leading CXs of every Cuccaro MAJ and
+    // the mirrored pair when uncomputing) into one swap pass.
+    {
+        std::vector<GRec> m;
+        m.reserve(recs.size());
+        std::vector<uint16_t> newidx(recs.size() + 1);
+        for (size_t j = 0; j < recs.size(); ++j) {
+            newidx[j] = (uint16_t)m.size();
+            const uint16_t c0 = recs[j].code;
+            if (j + 1 < recs.size() && c0 >= C_CX && c0 < C_CX + 25 && recs[j + 1].code >= C_CX &&
+                recs[j + 1].code < C_CX + 25) {
+                const int c = (c0 - C_CX) / 5, t1 = (c0 - C_CX) % 5;
+                const int c2 = (recs[j + 1].code - C_CX) / 5, t2 = (recs[j + 1].code - C_CX) % 5;
+                if (c == c2 && t1 != t2 && c != t1 && c != t2) {
+                    GRec r = recs[j];
+                    r.code = (uint16_t)(C_CX2 + 25 * c + 5 * std::min(t1, t2) + std::max(t1, t2));
+                    m.push_back(r);
+                    newidx[j + 1] = (uint16_t)m.size();
+                    ++j;
+                    continue;
+                }
+            }
+            m.push_back(recs[j]);
+        }
+        newidx[recs.size()] = (uint16_t)m.size();
+        for (auto &ph : phases) { ph.g0 = newidx[ph.g0]; ph.g1 = newidx[ph.g1]; }
+        recs.swap(m);
+    }
     // Coalescing: global loads/stores want lanes 0-2 on tile bits 0-2 (qubits 0,1,2: 128-byte
     // runs).  If the first (last) phase keeps one of those in a register, load (store) through an
     // extra layout phase and one shared-memory transpose instead (measured: 32 sectors per request,
