@@ -199,20 +199,22 @@ def main():
     B = args.leaves_per_step or max(1, min(nleaf, 64 if n >= 28 else 256))
     slots = np.zeros(cfg.shots, dtype=np.uint64)
 
-    # consecutive batches of the rank's DFS range; each step continues the traversal where the
-    # previous one stopped (TUSQ_EXEC_CONTINUE), wrapping to a fresh re-anchor at the range end
-    cursor = [lb]
+    # batches spread evenly over the rank's DFS range (the cost of a transition depends on where
+    # in the tree it is: early DFS leaves diverge late in the circuit); each batch starts with a
+    # re-anchor.  Warm-up batches come from the same spread, interleaved.
+    nb_total = args.warmup + (1 if args.full else args.steps)
+    stride = max(1, nleaf // max(nb_total, 1))
 
     def step(s, full=False):
-        b = lb if full else cursor[0]
+        b = lb if full else lb + (s * stride) % nleaf
         e = le if full else min(b + B, le)
-        f = flags | (T.EXEC_CONTINUE if (not full and b > lb) else 0)
-        _, st = T.run_tree(tree, prec, d_state=state, stream=stream, leaf_begin=b, leaf_end=e, flags=f,
+        _, st = T.run_tree(tree, prec, d_state=state, stream=stream, leaf_begin=b, leaf_end=e, flags=flags,
                            out_slots=slots)
-        cursor[0] = e if e < le else lb
         return st
 
-    for s in range(args.warmup):
+    order = list(range(nb_total))
+    warm, timed = order[1::2][:args.warmup], [s for s in order if s not in order[1::2][:args.warmup]]
+    for s in warm:
         step(s)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stats = []
@@ -222,7 +224,7 @@ def main():
     with Clocks(local) as clk:
         w0 = time.perf_counter()
         ev0.record(stream)
-        for s in range(1 if args.full else args.steps):
+        for s in ([0] if args.full else timed[:args.steps]):
             stats.append(step(s, args.full))
         ev1.record(stream)
         torch.cuda.synchronize()

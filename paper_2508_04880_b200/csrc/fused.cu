@@ -102,6 +102,7 @@ struct Params {
     uint16_t last_xpose;          // record index of the last transpose (0xFFFF: none)
     uint64_t regm_load;           // global mask of the phase-0 register qubits
     uint64_t gj[NR];              // global offset of tile-local index (j << NTB) (copy slots)
+    uint16_t sj[NR];              // swz(j << NTB): swizzled shared-memory part of copy slot j
     uint64_t gl[NR];              // phase 0: global element offset of register r (additive)
     uint64_t gs[NR];              // last phase: global element offset of register r (additive)
     Phase ph[MAXPH];
@@ -382,7 +383,9 @@ __device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const doub
 // shared-memory swizzle of a 12-bit tile index: the 16-byte slot's low 3 bits (its bank group
 // within a 128-byte wavefront) XOR a fold of the 9 high bits, so that the 8 lanes of a
 // quarter-warp hit distinct bank groups whichever 3 tile bits the lanes carry in a phase layout
-__device__ __forceinline__ uint32_t swz(uint32_t t) { return t ^ (((t >> 3) ^ (t >> 6) ^ (t >> 9)) & 7u); }
+// The swizzle is GF(2)-linear (swz(a ^ b) = swz(a) ^ swz(b)), so per-register parts are
+// swizzled on the host (Phase.so / so_out, Params.sj) and the kernel XORs one swizzled thread part.
+__host__ __device__ __forceinline__ uint32_t swz(uint32_t t) { return t ^ (((t >> 3) ^ (t >> 6) ^ (t >> 9)) & 7u); }
 
 template <int R_>
 __device__ __forceinline__ uint32_t roff32(const uint32_t (&rb)[RB])
@@ -423,7 +426,9 @@ __device__ __forceinline__ void prefetch_tile(V *sm, const V *psi, uint64_t T, c
 {
     const V *src = psi + (tile_base(T, P.qs) ^ P.xm_store) + gt;
 #pragma unroll
-    for (int j = 0; j < NR; ++j) cp_async<sizeof(V)>(sm + swz((tid + (uint32_t)NT * j) ^ P.mloc), src + P.gj[j]);
+    const uint32_t st = swz(tid ^ P.mloc);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) cp_async<sizeof(V)>(sm + (st ^ P.sj[j]), src + P.gj[j]);
     cp_async_commit();
 }
 
@@ -473,7 +478,9 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
 #pragma unroll
             for (int j = 0; j < NTB; ++j) t0 |= ((tid >> j) & 1u) << P.ph[0].tl[j];
 #pragma unroll
-            for (int r = 0; r < NR; ++r) a[r] = sm[swz(t0 | P.ph[0].so[r])];
+            t0 = swz(t0);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) a[r] = sm[t0 ^ P.ph[0].so[r]];
             if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: prefetch right away
                 __syncthreads();
                 if (Tn < P.ntiles) prefetch_tile(sm, psi, Tn, P, gt, tid);
@@ -500,7 +507,8 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
 #pragma unroll
                 for (int j = 0; j < NTB; ++j) tt |= ((tid >> j) & 1u) << prv.tl[j];
                 __syncthreads();
-#define TQ_ST(r) if constexpr (r < NR) sm[swz(tt | prv.so_out[r])] = a[r];
+                tt = swz(tt);
+#define TQ_ST(r) if constexpr (r < NR) sm[tt ^ prv.so_out[r]] = a[r];
                 TQ_ST(0) TQ_ST(1) TQ_ST(2) TQ_ST(3) TQ_ST(4) TQ_ST(5) TQ_ST(6) TQ_ST(7)
                 TQ_ST(8) TQ_ST(9) TQ_ST(10) TQ_ST(11) TQ_ST(12) TQ_ST(13) TQ_ST(14) TQ_ST(15)
                 TQ_ST(16) TQ_ST(17) TQ_ST(18) TQ_ST(19) TQ_ST(20) TQ_ST(21) TQ_ST(22) TQ_ST(23)
@@ -510,7 +518,8 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 tt = 0;
 #pragma unroll
                 for (int j = 0; j < NTB; ++j) tt |= ((tid >> j) & 1u) << cur.tl[j];
-#define TQ_LD(r) if constexpr (r < NR) a[r] = sm[swz(tt | cur.so[r])];
+                tt = swz(tt);
+#define TQ_LD(r) if constexpr (r < NR) a[r] = sm[tt ^ cur.so[r]];
                 TQ_LD(0) TQ_LD(1) TQ_LD(2) TQ_LD(3) TQ_LD(4) TQ_LD(5) TQ_LD(6) TQ_LD(7)
                 TQ_LD(8) TQ_LD(9) TQ_LD(10) TQ_LD(11) TQ_LD(12) TQ_LD(13) TQ_LD(14) TQ_LD(15)
                 TQ_LD(16) TQ_LD(17) TQ_LD(18) TQ_LD(19) TQ_LD(20) TQ_LD(21) TQ_LD(22) TQ_LD(23)
@@ -936,8 +945,8 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
             uint32_t o = 0;
             for (int k = 0; k < RB; ++k)
                 if (r & (1 << k)) o |= 1u << ph.rl[k];
-            ph.so[r] = (uint16_t)o;
-            ph.so_out[r] = (uint16_t)o;
+            ph.so[r] = (uint16_t)swz(o);        // pre-swizzled (swz is linear)
+            ph.so_out[r] = (uint16_t)swz(o);
         }
         return ph;
     };
@@ -1375,6 +1384,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 for (int k = 0; k < RB; ++k)
                     if (j & (1 << k)) o |= bit(P.qs[NTB + k]);
                 P.gj[j] = o;
+                P.sj[j] = (uint16_t)swz((uint32_t)j << NTB);
             }
             P.last_xpose = 0xFFFFu;
             for (uint32_t i = 0; i < P.ngate; ++i)
