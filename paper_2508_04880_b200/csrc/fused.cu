@@ -629,17 +629,20 @@ void GateTimer::begin(cudaStream_t st)
     cudaEventRecord(a_[used_], st);
 }
 
-void GateTimer::end(cudaStream_t st, double bytes)
+void GateTimer::end(cudaStream_t st, double bytes, const char *tag)
 {
     if (!on_) return;
     cudaEventRecord(b_[used_], st);
     by_[used_] = bytes;
+    if (tags_.size() <= used_) tags_.resize(used_ + 1);
+    tags_[used_] = tag ? tag : "";
     ++used_;
 }
 
 void GateTimer::flush()
 {
     if (!on_ || !used_) return;
+    static const bool trace = getenv("TUSQ_TRACE_LAUNCHES") != nullptr;
     cudaEventSynchronize(b_[used_ - 1]);
     for (size_t i = 0; i < used_; ++i) {
         float ms = 0;
@@ -647,6 +650,7 @@ void GateTimer::flush()
         seconds += ms * 1e-3;
         bytes += by_[i];
         ++launches;
+        if (trace) fprintf(stderr, "[launch] %.3f ms %s\n", ms, tags_[i].c_str());
     }
     used_ = 0;
 }
@@ -1419,7 +1423,24 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 k_fused<double><<<(unsigned)grid, NT, smem, ctx.st>>>((double2 *)ctx.psi, P, d_sums);
             else
                 k_fused<float><<<(unsigned)grid, NT, smem, ctx.st>>>((float2 *)ctx.psi, P, d_sums);
-            if (ctx.timer) ctx.timer->end(ctx.st, bytes);
+            if (ctx.timer) {
+                static const bool trace = getenv("TUSQ_TRACE_LAUNCHES") != nullptr;
+                char tag[160] = "";
+                if (trace) {
+                    int cnt[8] = {0};   // H, DK, CX/CX2, D1/D2, XPOSE, X/Y, T*, other
+                    for (uint32_t i = 0; i < P.ngate; ++i) {
+                        const uint16_t c = P.g[i].code;
+                        int k = c < C_U ? 0 : (c >= C_DK && c < C_CX2) ? 1 : ((c >= C_CX && c < C_CPH) || (c >= C_CX2 && c < C_N)) ? 2
+                                : (c >= C_D1 && c < C_CX) ? 3 : c == C_XPOSE ? 4 : (c >= C_X && c < C_D1) ? 5
+                                : (c >= C_TX && c <= C_TPH) ? 6 : 7;
+                        cnt[k]++;
+                    }
+                    snprintf(tag, sizeof(tag), "ops %zu recs %u ph %u init %d tile %#llx H%d DK%d CX%d D%d XP%d XY%d T%d O%d",
+                             G.ops.size(), P.ngate, P.nphase, pending_init ? 1 : 0, (unsigned long long)B.tile, cnt[0],
+                             cnt[1], cnt[2], cnt[3], cnt[4], cnt[5], cnt[6], cnt[7]);
+                }
+                ctx.timer->end(ctx.st, bytes, tag);
+            }
         }
         count(ctx, bytes, true);
         pending_init = false;

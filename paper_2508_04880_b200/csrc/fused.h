@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <string>
 #include <vector>
 
 #include "common.h"
@@ -15,7 +16,7 @@ public:
     ~GateTimer();
     bool on() const { return on_; }
     void begin(cudaStream_t st);
-    void end(cudaStream_t st, double bytes);
+    void end(cudaStream_t st, double bytes, const char *tag = nullptr);
     void flush();                 // synchronizes the recorded events and accumulates
     uint64_t launches = 0;
     double seconds = 0.0, bytes = 0.0;
@@ -24,6 +25,7 @@ private:
     bool on_;
     std::vector<cudaEvent_t> a_, b_;
     std::vector<double> by_;
+    std::vector<std::string> tags_;
     size_t used_ = 0;
 };
 

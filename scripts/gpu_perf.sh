@@ -11,3 +11,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fused -s ${NCU_SKIP:-12} -c 1 -o $O/prof_fused \
   python bench.py --steps 1 --warmup 3 --leaves-per-step 64 --no-cpu-baseline > $O/ncu_full.log 2>&1
 echo done
+# the isolated Adder MAJ group (kernel microbench K5) under a full capture
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 0 -c 1 -o $O/prof_maj \
+  python scripts/kernel_bench.py > $O/ncu_maj.log 2>&1
+echo done2
