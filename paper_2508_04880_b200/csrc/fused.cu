@@ -1170,6 +1170,51 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         for (auto &ph : phases) { ph.g0 = newidx[ph.g0]; ph.g1 = newidx[ph.g1]; }
         recs.swap(m);
     }
+    // Split a phase right after an interior run of >= 2 register-permutation records (e.g. the
+    // two trailing CXs of every Cuccaro UMA): the run then ends its phase and is absorbed into the
+    // transpose that follows (same register set), trading ~2 swap passes for one transpose.
+    {
+        std::vector<GRec> out;
+        std::vector<Phase> nph;
+        out.reserve(recs.size() + 8);
+        for (size_t p = 0; p < phases.size(); ++p) {
+            Phase ph = phases[p];
+            if (p > 0) {
+                GRec x = recs[ph.g0 - 1];   // the transpose entering this phase
+                x.a = (uint8_t)nph.size();
+                out.push_back(x);
+            }
+            const size_t g0 = ph.g0, g1 = ph.g1;
+            ph.g0 = (uint16_t)out.size();
+            size_t j = g0;
+            while (j < g1) {
+                size_t k = j;
+                while (k < g1 && is_perm_rec(recs[k].code)) ++k;
+                const bool interior = j > g0 && k < g1;
+                if (k - j >= 2 && interior && nph.size() + (phases.size() - p) < (size_t)MAXPH - 2) {
+                    for (size_t q = j; q < k; ++q) out.push_back(recs[q]);
+                    ph.g1 = (uint16_t)out.size();
+                    nph.push_back(ph);
+                    GRec x;
+                    memset(&x, 0, sizeof(x));
+                    x.code = C_XPOSE;
+                    x.a = (uint8_t)nph.size();
+                    out.push_back(x);
+                    Phase cont = phases[p];   // same register set and layout
+                    cont.g0 = (uint16_t)out.size();
+                    ph = cont;
+                    j = k;
+                    continue;
+                }
+                if (k == j) { out.push_back(recs[j]); ++j; }
+                else { for (size_t q = j; q < k; ++q) out.push_back(recs[q]); j = k; }
+            }
+            ph.g1 = (uint16_t)out.size();
+            nph.push_back(ph);
+        }
+        recs.swap(out);
+        phases.swap(nph);
+    }
     // Coalescing: global loads/stores want lanes 0-2 on tile bits 0-2 (qubits 0,1,2: 128-byte
     // runs).  If the first (last) phase keeps one of those in a register, load (store) through an
     // extra layout phase and one shared-memory transpose instead (measured: 32 sectors per request,

@@ -32,7 +32,9 @@ KEYS = {
 def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[0]
+    hdr, units = rows[0], dict(zip(rows[0], rows[1]))
+    scale = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6,
+             "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     res = []
     for r in rows[2:]:
         d = dict(zip(hdr, r))
@@ -40,7 +42,7 @@ def raw(rep):
         for k, name in KEYS.items():
             if k in d and d[k] not in ("", "n/a"):
                 try:
-                    e[name] = float(d[k].replace(",", ""))
+                    e[name] = float(d[k].replace(",", "")) * scale.get(units.get(k, ""), 1)
                 except ValueError:
                     e[name] = d[k]
         res.append(e)
