@@ -506,7 +506,9 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 uint32_t tt = 0;
 #pragma unroll
                 for (int j = 0; j < NTB; ++j) tt |= ((tid >> j) & 1u) << prv.tl[j];
-                __syncthreads();
+                // g.b = 1: same thread-bit layout on both sides -- every thread writes and reads
+                // back only its own slots (a register permutation), no barrier needed
+                if (!g.b) __syncthreads();
                 tt = swz(tt);
 #define TQ_ST(r) if constexpr (r < NR) sm[tt ^ prv.so_out[r]] = a[r];
                 TQ_ST(0) TQ_ST(1) TQ_ST(2) TQ_ST(3) TQ_ST(4) TQ_ST(5) TQ_ST(6) TQ_ST(7)
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 TQ_ST(16) TQ_ST(17) TQ_ST(18) TQ_ST(19) TQ_ST(20) TQ_ST(21) TQ_ST(22) TQ_ST(23)
                 TQ_ST(24) TQ_ST(25) TQ_ST(26) TQ_ST(27) TQ_ST(28) TQ_ST(29) TQ_ST(30) TQ_ST(31)
 #undef TQ_ST
-                __syncthreads();
+                if (!g.b) __syncthreads();
                 tt = 0;
 #pragma unroll
                 for (int j = 0; j < NTB; ++j) tt |= ((tid >> j) & 1u) << cur.tl[j];
@@ -1297,6 +1299,15 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         throw std::runtime_error("fused planner: group exceeds the kernel parameter block");
     P.nphase = (uint32_t)phases.size();
     P.ngate = (uint32_t)recs.size();
+    // transposes between phases with identical thread-bit layouts are thread-local (no barrier)
+    {
+        uint32_t cur = 0;
+        for (auto &r : recs) {
+            if (r.code != C_XPOSE) continue;
+            r.b = memcmp(phases[cur].tl, phases[r.a].tl, NTB) == 0 ? 1 : 0;
+            cur = r.a;
+        }
+    }
     static const bool dbg = getenv("TUSQ_DEBUG_PLAN") != nullptr;
     static const bool sigs = getenv("TUSQ_DEBUG_SIGS") != nullptr;
     if (sigs) {
