@@ -289,18 +289,14 @@ __device__ __forceinline__ void g_cph(V (&a)[NR], R pr, R pi)
 template <int M, typename V, typename R>
 __device__ __forceinline__ void g_dk(V (&a)[NR], const double *tab)
 {
-    // one warp-uniform branch per table entry: entries equal to 1 (about half of a Toffoli core's
-    // phase table) cost nothing
+    // straight-line: the 2^k table entries are loaded up front, then 32 independent complex
+    // multiplies (per-entry "skip if 1" branches were measured slower: they serialize the warp)
     constexpr int K = __builtin_popcount(M);
+    R tr[1 << K], ti[1 << K];
 #pragma unroll
-    for (int idx = 0; idx < (1 << K); ++idx) {
-        const R pr = (R)tab[2 * idx], pi = (R)tab[2 * idx + 1];
-        if (pr != R(1) || pi != R(0)) {
+    for (int idx = 0; idx < (1 << K); ++idx) { tr[idx] = (R)tab[2 * idx]; ti[idx] = (R)tab[2 * idx + 1]; }
 #pragma unroll
-            for (int i = 0; i < NR; ++i)
-                if (pext5(i, M) == idx) cmul_ip(a[i], pr, pi);
-        }
-    }
+    for (int i = 0; i < NR; ++i) cmul_ip(a[i], tr[pext5(i, M)], ti[pext5(i, M)]);
 }
 
 // One gate record.  C is a compile-time code; the dispatch below is a balanced binary tree of
@@ -377,7 +373,12 @@ __device__ __forceinline__ void dispatch(int code, V (&a)[NR], const double *p, 
 template <typename V, typename R>
 __device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const double *prm, uint64_t lbase)
 {
-    dispatch<0, C_N, V, R>(g.code, a, prm + g.pi, lbase, g.a, g.b);
+    // fast paths for the two hottest classes (H and diagonal tables: ~2/3 of all records)
+    const int c = g.code;
+    if (c < C_U) dispatch<0, C_U, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else if (c >= C_DK && c < C_DK + NR) dispatch<C_DK, C_DK + NR, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else if (c < C_DK) dispatch<C_U, C_DK, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else dispatch<C_CX2, C_N, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
 }
 
 // shared-memory swizzle of a 12-bit tile index: the 16-byte slot's low 3 bits (its bank group
@@ -494,8 +495,19 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
         uint64_t lbase = base;
 #pragma unroll
         for (int j = 0; j < NTB; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[P.ph[0].tl[j]];
+        // records are fetched as one 64-bit constant load, one record ahead (the fetch -> decode
+        // -> branch chain was the top stall in ncu's source view)
+        const uint64_t *recw = reinterpret_cast<const uint64_t *>(P.g);
+        uint64_t wnext = P.ngate ? recw[0] : 0;
         for (uint32_t gi = 0; gi < P.ngate; ++gi) {
-            const GRec g = P.g[gi];
+            const uint64_t w = wnext;
+            wnext = recw[gi + 1 < P.ngate ? gi + 1 : gi];
+            GRec g;
+            g.code = (uint16_t)w;
+            g.a = (uint8_t)(w >> 16);
+            g.b = (uint8_t)(w >> 24);
+            g.pi = (uint16_t)(w >> 32);
+            g._pad = 0;
             if (g.code != C_XPOSE) {
                 apply_gate<V, R>(a, g, P.prm, lbase);
             } else {
@@ -1172,6 +1184,10 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         for (auto &ph : phases) { ph.g0 = newidx[ph.g0]; ph.g1 = newidx[ph.g1]; }
         recs.swap(m);
     }
+    // Tunables (environment, for measurement): TUSQ_SPLIT_MIN (>= 2 enables phase splits after
+    // permutation runs), TUSQ_STORE_XPOSE=1 (coalescing transpose before the store).
+    static const size_t split_min = getenv("TUSQ_SPLIT_MIN") ? (size_t)atoi(getenv("TUSQ_SPLIT_MIN")) : 1000;
+    static const bool store_xpose = getenv("TUSQ_STORE_XPOSE") && getenv("TUSQ_STORE_XPOSE")[0] == '1';
     // Split a phase right after an interior run of >= 2 register-permutation records (e.g. the
     // two trailing CXs of every Cuccaro UMA): the run then ends its phase and is absorbed into the
     // transpose that follows (same register set), trading ~2 swap passes for one transpose.
@@ -1193,7 +1209,10 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                 size_t k = j;
                 while (k < g1 && is_perm_rec(recs[k].code)) ++k;
                 const bool interior = j > g0 && k < g1;
-                if (k - j >= 2 && interior && nph.size() + (phases.size() - p) < (size_t)MAXPH - 2) {
+                // measured (launch traces, least squares): a transpose costs ~1.3 ms per 30-qubit
+                // sweep (a full shared-memory pass is >= 0.93 ms at 37 TB/s) vs ~0.5 ms per swap
+                // record, so split only for runs of >= split_min records (default: never)
+                if (k - j >= split_min && interior && nph.size() + (phases.size() - p) < (size_t)MAXPH - 2) {
                     for (size_t q = j; q < k; ++q) out.push_back(recs[q]);
                     ph.g1 = (uint16_t)out.size();
                     nph.push_back(ph);
@@ -1245,7 +1264,7 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
             recs.insert(recs.begin(), x);
             phases.insert(phases.begin(), c);
         }
-        if (low_in_regs(phases.back())) {
+        if (store_xpose && low_in_regs(phases.back())) {
             GRec x;
             memset(&x, 0, sizeof(x));
             x.code = C_XPOSE;
