@@ -59,9 +59,24 @@ enum Code : uint16_t {
     C_TPH = 90,   //         all *= pred(q0)&pred(q1) ? p1 : p0 (4 params)
     C_DK = 91,    // +mask   a[r] *= tab[pext(r, mask)]  (2 * 2^popc(mask) params)
     C_CX2 = 123,  // +25c+5t1+t2 (t1 < t2): CX(c->t1) CX(c->t2) as ONE swap pass
-    C_N = 248,    // number of gate codes
-    C_XPOSE = 248 // transpose registers to phase a
+    C_CU = 248,   // +6p+j   2x2 on bit p per pattern of the control pair j (Toffoli cores), 32 params
+    C_N = 278,    // number of gate codes
+    C_XPOSE = 278 // transpose registers to phase a
 };
+
+// the j-th (0..5) pair {u < v} of register bits other than p, as a mask (with p): the diagonal of a
+// Toffoli core H(t) DK(a, b, t) H(t)
+__host__ __device__ constexpr int hdh_mask(int p, int j)
+{
+    int k = 0;
+    for (int u = 0; u < 5; ++u)
+        for (int v = u + 1; v < 5; ++v) {
+            if (u == p || v == p) continue;
+            if (k == j) return (1 << p) | (1 << u) | (1 << v);
+            ++k;
+        }
+    return 0;
+}
 
 __host__ __device__ constexpr int pext5(int r, int m)
 {
@@ -299,6 +314,79 @@ __device__ __forceinline__ void g_dk(V (&a)[NR], const double *tab)
     for (int i = 0; i < NR; ++i) cmul_ip(a[i], tr[pext5(i, M)], ti[pext5(i, M)]);
 }
 
+// new (x, y) = (m00 x + m01 y, m10 x + m11 y), in place
+__device__ __forceinline__ void mat2_ip(double2 &x, double2 &y, const double *m)
+{
+    asm volatile("{\n\t.reg .f64 a, b, c, d;\n\t"
+                 "mul.f64 a, %4, %0;\n\tneg.f64 b, %5;\n\tfma.rn.f64 a, b, %1, a;\n\t"
+                 "neg.f64 d, %7;\n\tfma.rn.f64 a, d, %3, a;\n\tfma.rn.f64 a, %6, %2, a;\n\t"
+                 "mul.f64 b, %4, %1;\n\tfma.rn.f64 b, %5, %0, b;\n\tfma.rn.f64 b, %6, %3, b;\n\tfma.rn.f64 b, %7, %2, b;\n\t"
+                 "mul.f64 c, %8, %0;\n\tneg.f64 d, %9;\n\tfma.rn.f64 c, d, %1, c;\n\tfma.rn.f64 c, %10, %2, c;\n\t"
+                 "neg.f64 d, %11;\n\tfma.rn.f64 c, d, %3, c;\n\t"
+                 "mul.f64 d, %8, %1;\n\tfma.rn.f64 d, %9, %0, d;\n\tfma.rn.f64 d, %10, %3, d;\n\tfma.rn.f64 d, %11, %2, d;\n\t"
+                 "mov.f64 %0, a;\n\tmov.f64 %1, b;\n\tmov.f64 %2, c;\n\tmov.f64 %3, d;\n\t}"
+                 : "+d"(x.x), "+d"(x.y), "+d"(y.x), "+d"(y.y)
+                 : "d"(m[0]), "d"(m[1]), "d"(m[2]), "d"(m[3]), "d"(m[4]), "d"(m[5]), "d"(m[6]), "d"(m[7]));
+}
+__device__ __forceinline__ void mat2_ip(float2 &x, float2 &y, const double *md)
+{
+    const float m0 = (float)md[0], m1 = (float)md[1], m2 = (float)md[2], m3 = (float)md[3];
+    const float m4 = (float)md[4], m5 = (float)md[5], m6 = (float)md[6], m7 = (float)md[7];
+    asm volatile("{\n\t.reg .f32 a, b, c, d;\n\t"
+                 "mul.f32 a, %4, %0;\n\tneg.f32 b, %5;\n\tfma.rn.f32 a, b, %1, a;\n\t"
+                 "neg.f32 d, %7;\n\tfma.rn.f32 a, d, %3, a;\n\tfma.rn.f32 a, %6, %2, a;\n\t"
+                 "mul.f32 b, %4, %1;\n\tfma.rn.f32 b, %5, %0, b;\n\tfma.rn.f32 b, %6, %3, b;\n\tfma.rn.f32 b, %7, %2, b;\n\t"
+                 "mul.f32 c, %8, %0;\n\tneg.f32 d, %9;\n\tfma.rn.f32 c, d, %1, c;\n\tfma.rn.f32 c, %10, %2, c;\n\t"
+                 "neg.f32 d, %11;\n\tfma.rn.f32 c, d, %3, c;\n\t"
+                 "mul.f32 d, %8, %1;\n\tfma.rn.f32 d, %9, %0, d;\n\tfma.rn.f32 d, %10, %3, d;\n\tfma.rn.f32 d, %11, %2, d;\n\t"
+                 "mov.f32 %0, a;\n\tmov.f32 %1, b;\n\tmov.f32 %2, c;\n\tmov.f32 %3, d;\n\t}"
+                 : "+f"(x.x), "+f"(x.y), "+f"(y.x), "+f"(y.y)
+                 : "f"(m0), "f"(m1), "f"(m2), "f"(m3), "f"(m4), "f"(m5), "f"(m6), "f"(m7));
+}
+
+// Controlled 2x2 on bit P: for each pattern b of the control bits CM, the block of amplitude
+// pairs (bit P = 0, 1) gets the matrix m[8b .. 8b+7] (m00, m01, m10, m11 complex).  The host
+// classifies each block (2 bits of `kinds` per block): 0 identity (skipped), 1 diagonal,
+// 2 anti-diagonal (swap, then the two entries unless bit b of `unit` says they are 1), 3 general.
+// This is H(t) DK(a, b, t) H(t) DK(a, b) -- a Toffoli core with its control phases -- which for a
+// Toffoli is the identity on three blocks and a plain swap on the fourth.
+template <int P, int CM, typename V, typename R>
+__device__ __forceinline__ void g_cu(V (&a)[NR], const double *m, uint32_t kinds, uint32_t unit)
+{
+    constexpr int NB = 1 << __builtin_popcount(CM);
+#pragma unroll
+    for (int bi = 0; bi < NB; ++bi) {
+        const uint32_t kd = (kinds >> (2 * bi)) & 3u;
+        const double *q = m + 8 * bi;
+        if (kd == 1) {
+            const R d0r = (R)q[0], d0i = (R)q[1], d1r = (R)q[6], d1i = (R)q[7];
+#pragma unroll
+            for (int i = 0; i < NR; ++i)
+                if (!(i & (1 << P)) && pext5(i, CM) == bi) {
+                    cmul_ip(a[i], d0r, d0i);
+                    cmul_ip(a[i | (1 << P)], d1r, d1i);
+                }
+        } else if (kd == 2) {
+#pragma unroll
+            for (int i = 0; i < NR; ++i)
+                if (!(i & (1 << P)) && pext5(i, CM) == bi) vswap(a[i], a[i | (1 << P)]);
+            if (!((unit >> bi) & 1u)) {
+                const R xr = (R)q[2], xi = (R)q[3], yr = (R)q[4], yi = (R)q[5];
+#pragma unroll
+                for (int i = 0; i < NR; ++i)
+                    if (!(i & (1 << P)) && pext5(i, CM) == bi) {
+                        cmul_ip(a[i], xr, xi);
+                        cmul_ip(a[i | (1 << P)], yr, yi);
+                    }
+            }
+        } else if (kd == 3) {
+#pragma unroll
+            for (int i = 0; i < NR; ++i)
+                if (!(i & (1 << P)) && pext5(i, CM) == bi) mat2_ip(a[i], a[i | (1 << P)], q);
+        }
+    }
+}
+
 // One gate record.  C is a compile-time code; the dispatch below is a balanced binary tree of
 // compile-time ranges (7 compare-and-branch levels) instead of the linear compare chain ptxas
 // emits for a 123-way switch.
@@ -311,6 +399,7 @@ __host__ __device__ constexpr bool code_ok(int C)
     if (C < C_TPH) return (C - C_TX) % 5 < RB;
     if (C == C_TPH) return true;
     if (C < C_CX2) return C - C_DK < NR;
+    if (C >= C_CU) return hdh_mask((C - C_CU) / 6, (C - C_CU) % 6) < NR;
     const int c = (C - C_CX2) / 25, t1 = (C - C_CX2) / 5 % 5, t2 = (C - C_CX2) % 5;
     return c < RB && t1 < RB && t2 < RB && t1 < t2 && c != t1 && c != t2;
 }
@@ -349,6 +438,9 @@ __device__ __forceinline__ void gate_case(V (&a)[NR], const double *p, uint64_t 
 #pragma unroll
             for (int i = 0; i < NR; ++i) cmul_ip(a[i], fr, fi);
         }
+    } else if constexpr (C >= C_CU) {
+        constexpr int pb = (C - C_CU) / 6;
+        g_cu<pb, hdh_mask(pb, (C - C_CU) % 6) & ~(1 << pb), V, R>(a, p, gb, ga);
     } else if constexpr (C >= C_CX2) {
         constexpr int c = (C - C_CX2) / 25, t1 = (C - C_CX2) / 5 % 5, t2 = (C - C_CX2) % 5;
         g_cx2<c, t1, t2>(a);
@@ -378,7 +470,8 @@ __device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const doub
     if (c < C_U) dispatch<0, C_U, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
     else if (c >= C_DK && c < C_DK + NR) dispatch<C_DK, C_DK + NR, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
     else if (c < C_DK) dispatch<C_U, C_DK, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
-    else dispatch<C_CX2, C_N, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else if (c >= C_CU) dispatch<C_CU, C_N, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else dispatch<C_CX2, C_CU, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
 }
 
 // shared-memory swizzle of a 12-bit tile index: the 16-byte slot's low 3 bits (its bank group
@@ -496,7 +589,8 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
 #pragma unroll
         for (int j = 0; j < NTB; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[P.ph[0].tl[j]];
         // records are fetched as one 64-bit constant load, one record ahead (the fetch -> decode
-        // -> branch chain was the top stall in ncu's source view)
+        // -> branch chain was the top stall in ncu's source view; a shared-memory copy fetched by
+        // a volatile load at the top of the iteration measured ~6 % slower)
         const uint64_t *recw = reinterpret_cast<const uint64_t *>(P.g);
         uint64_t wnext = P.ngate ? recw[0] : 0;
         for (uint32_t gi = 0; gi < P.ngate; ++gi) {
@@ -835,13 +929,28 @@ struct Built {
     uint64_t tile = 0;
     uint8_t pin0[NR];      // absorbed entry permutation of phase 0: register r reads pattern pin0[r]
     uint8_t pout_last[NR]; // absorbed exit permutation of the last phase: register s written as pattern pout[s]
+    int h_absorbed = 0;    // H's folded into C_CU records (exactly scaled there)
 };
+
+// parameter doubles a record reads at prm[pi]
+static int rec_nparams(uint16_t c)
+{
+    if (c >= C_U && c < C_X) return 8;
+    if (c >= C_D1 && c < C_D2) return 2;
+    if (c >= C_D2 && c < C_CX) return 4;
+    if (c >= C_CPH && c < C_TX) return 2;
+    if (c >= C_TD1 && c < C_TPH) return 2;
+    if (c == C_TPH) return 4;
+    if (c >= C_DK && c < C_CX2) return 2 << __builtin_popcount(c - C_DK);
+    if (c >= C_CU && c < C_N) return 32;
+    return 0;
+}
 
 static bool is_perm_rec(uint16_t c)
 {
     if (c >= C_X && c < C_X + 5) return true;
     if (c >= C_CX && c < C_CX + 25) return (c - C_CX) / 5 != (c - C_CX) % 5;
-    if (c >= C_CX2 && c < C_N) return code_ok(c);
+    if (c >= C_CX2 && c < C_CU) return code_ok(c);
     return false;
 }
 
@@ -1184,6 +1293,97 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         for (auto &ph : phases) { ph.g0 = newidx[ph.g0]; ph.g1 = newidx[ph.g1]; }
         recs.swap(m);
     }
+    // Toffoli cores: H(t) DK(a, b, t) H(t) [DK(subset of a, b)] is, per pattern of the controls
+    // (a, b), a 2x2 matrix on t -- ONE controlled-2x2 record (C_CU) replaces 3-4 records.  The host
+    // multiplies the blocks out exactly as the gates define them (the two H's included, so the
+    // group's deferred (1/sqrt2)^h drops 2 per merge) and classifies each block: for an error-free
+    // Toffoli three blocks are the identity and the fourth is a plain swap.
+    B.h_absorbed = 0;
+    {
+        static const bool no_cu = getenv("TUSQ_NO_CU") != nullptr;
+        std::vector<GRec> m;
+        m.reserve(recs.size());
+        std::vector<uint16_t> newidx(recs.size() + 1);
+        for (size_t j = 0; j < recs.size(); ++j) {
+            newidx[j] = (uint16_t)m.size();
+            const uint16_t c0 = recs[j].code;
+            if (!no_cu && j + 2 < recs.size() && c0 < C_H + RB && recs[j + 2].code == c0 && recs[j + 1].code >= C_DK &&
+                recs[j + 1].code < C_DK + NR) {
+                const int p = c0 - C_H, mask = recs[j + 1].code - C_DK;
+                int jj = -1;
+                for (int q = 0; q < 6; ++q)
+                    if (hdh_mask(p, q) == mask) jj = q;
+                if (jj >= 0 && code_ok(C_CU + 6 * p + jj)) {
+                    const int cm = mask & ~(1 << p);
+                    const double *t1 = &prm[recs[j + 1].pi];
+                    // optional trailing diagonal on the controls
+                    const double *t2 = nullptr;
+                    int m2 = 0;
+                    if (j + 3 < recs.size() && recs[j + 3].code > C_DK && recs[j + 3].code < C_DK + NR &&
+                        ((recs[j + 3].code - C_DK) & ~cm) == 0) {
+                        m2 = recs[j + 3].code - C_DK;
+                        t2 = &prm[recs[j + 3].pi];
+                    }
+                    auto pextm = [](uint32_t x, uint32_t mk) {
+                        uint32_t o = 0, k = 0;
+                        for (int b = 0; b < RB; ++b)
+                            if (mk & (1u << b)) { o |= ((x >> b) & 1u) << k; ++k; }
+                        return o;
+                    };
+                    std::vector<double> blk(32, 0.0);
+                    uint32_t kinds = 0, unit = 0;
+                    for (uint32_t bi = 0; bi < 4; ++bi) {
+                        uint32_t x = 0, k = 0;   // deposit bi into the control bits
+                        for (int b = 0; b < RB; ++b)
+                            if (cm & (1 << b)) { if ((bi >> k) & 1u) x |= 1u << b; ++k; }
+                        const uint32_t x0 = x, x1 = x | (1u << p);
+                        const double d0r = t1[2 * pextm(x0, mask)], d0i = t1[2 * pextm(x0, mask) + 1];
+                        const double d1r = t1[2 * pextm(x1, mask)], d1i = t1[2 * pextm(x1, mask) + 1];
+                        double fr = 1.0, fi = 0.0;
+                        if (t2) { fr = t2[2 * pextm(x0, m2)]; fi = t2[2 * pextm(x0, m2) + 1]; }
+                        // (1/2) [[d0 + d1, d0 - d1], [d0 - d1, d0 + d1]] * f   (= H diag(d0, d1) H, then f)
+                        const double sr = 0.5 * (d0r + d1r), si = 0.5 * (d0i + d1i);
+                        const double ar = 0.5 * (d0r - d1r), ai = 0.5 * (d0i - d1i);
+                        double e[8] = {sr * fr - si * fi, sr * fi + si * fr, ar * fr - ai * fi, ar * fi + ai * fr,
+                                       ar * fr - ai * fi, ar * fi + ai * fr, sr * fr - si * fi, sr * fi + si * fr};
+                        // snap to the exact values the algebra gives (errors <= a few ulp)
+                        for (double &v : e) {
+                            if (fabs(v) < 1e-15) v = 0.0;
+                            else if (fabs(v - 1.0) < 4e-16) v = 1.0;
+                            else if (fabs(v + 1.0) < 4e-16) v = -1.0;
+                        }
+                        const bool offz = e[2] == 0 && e[3] == 0 && e[4] == 0 && e[5] == 0;
+                        const bool diagz = e[0] == 0 && e[1] == 0 && e[6] == 0 && e[7] == 0;
+                        uint32_t kd = 3;
+                        if (offz) kd = (e[0] == 1 && e[1] == 0 && e[6] == 1 && e[7] == 0) ? 0 : 1;
+                        else if (diagz) {
+                            kd = 2;
+                            if (e[2] == 1 && e[3] == 0 && e[4] == 1 && e[5] == 0) unit |= 1u << bi;
+                        }
+                        kinds |= kd << (2 * bi);
+                        for (int q = 0; q < 8; ++q) blk[8 * bi + q] = e[q];
+                    }
+                    GRec r;
+                    memset(&r, 0, sizeof(r));
+                    r.code = (uint16_t)(C_CU + 6 * p + jj);
+                    r.a = (uint8_t)unit;
+                    r.b = (uint8_t)kinds;
+                    r.pi = (uint16_t)prm.size();
+                    prm.insert(prm.end(), blk.begin(), blk.end());
+                    m.push_back(r);
+                    B.h_absorbed += 2;
+                    const size_t used = t2 ? 4 : 3;
+                    for (size_t q = 1; q < used; ++q) newidx[j + q] = (uint16_t)m.size();
+                    j += used - 1;
+                    continue;
+                }
+            }
+            m.push_back(recs[j]);
+        }
+        newidx[recs.size()] = (uint16_t)m.size();
+        for (auto &ph : phases) { ph.g0 = newidx[ph.g0]; ph.g1 = newidx[ph.g1]; }
+        recs.swap(m);
+    }
     // Tunables (environment, for measurement): TUSQ_SPLIT_MIN (>= 2 enables phase splits after
     // permutation runs), TUSQ_STORE_XPOSE=1 (coalescing transpose before the store).
     static const size_t split_min = getenv("TUSQ_SPLIT_MIN") ? (size_t)atoi(getenv("TUSQ_SPLIT_MIN")) : 1000;
@@ -1314,6 +1514,18 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         }
         recs.swap(kept);
     }
+    {   // compact the parameter block (merges leave their inputs' parameters unused)
+        std::vector<double> used;
+        used.reserve(prm.size());
+        for (auto &r : recs) {
+            const int np = rec_nparams(r.code);
+            if (!np) continue;
+            const uint16_t at = (uint16_t)used.size();
+            used.insert(used.end(), prm.begin() + r.pi, prm.begin() + r.pi + np);
+            r.pi = at;
+        }
+        prm.swap(used);
+    }
     if (phases.size() > (size_t)MAXPH || recs.size() > (size_t)MAXG || prm.size() > (size_t)MAXP)
         throw std::runtime_error("fused planner: group exceeds the kernel parameter block");
     P.nphase = (uint32_t)phases.size();
@@ -1342,6 +1554,12 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
             for (auto &k : G.ops) fprintf(stderr, " %u(%u,%u)", k.op.kind, k.op.q0, k.op.q1);
             fprintf(stderr, "\n  codes:");
             for (auto &r : recs) fprintf(stderr, " %u", r.code);
+            for (auto &r : recs)
+                if (r.code >= C_DK && r.code < C_CX2) {
+                    fprintf(stderr, "\n  dk %u:", r.code - C_DK);
+                    for (int e = 0; e < (2 << __builtin_popcount(r.code - C_DK)); ++e)
+                        fprintf(stderr, " %.3f", prm[r.pi + e]);
+                }
             fprintf(stderr, "\n  phases:");
             for (auto &ph : phases) {
                 fprintf(stderr, " [g%u-%u regs", ph.g0, ph.g1);
@@ -1480,6 +1698,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         double sc = 1.0;
         int nh = 0;
         for (auto &k : G.ops) nh += k.op.kind == H;
+        nh -= B.h_absorbed;
         for (int i = 0; i < nh / 2; ++i) sc *= 0.5;
         if (nh & 1) sc *= M_SQRT1_2;
         P.scale_re = sc * G.fr;
@@ -1505,7 +1724,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                     int cnt[8] = {0};   // H, DK, CX/CX2, D1/D2, XPOSE, X/Y, T*, other
                     for (uint32_t i = 0; i < P.ngate; ++i) {
                         const uint16_t c = P.g[i].code;
-                        int k = c < C_U ? 0 : (c >= C_DK && c < C_CX2) ? 1 : ((c >= C_CX && c < C_CPH) || (c >= C_CX2 && c < C_N)) ? 2
+                        int k = c < C_U ? 0 : (c >= C_DK && c < C_CX2) ? 1 : ((c >= C_CX && c < C_CPH) || (c >= C_CX2 && c < C_CU)) ? 2
                                 : (c >= C_D1 && c < C_CX) ? 3 : c == C_XPOSE ? 4 : (c >= C_X && c < C_D1) ? 5
                                 : (c >= C_TX && c <= C_TPH) ? 6 : 7;
                         cnt[k]++;
