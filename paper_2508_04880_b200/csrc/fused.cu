@@ -1172,8 +1172,39 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         return true;
     };
     std::vector<double> ftab;
+    // Phase switches are moved back to the start of a Toffoli core: when op i needs a switch and
+    // the ops since the last H(t) -- or since the H(t) before it, H(t) run H(t) -- are all
+    // classical, the records from that H on are dropped and re-planned in the new phase, so that
+    // the core folds into one table (and one C_CU record) instead of being cut in two.
+    static const bool no_backup = getenv("TUSQ_NO_BACKUP") != nullptr;
+    std::vector<size_t> rec_at(G.ops.size(), SIZE_MAX), prm_at(G.ops.size(), SIZE_MAX);
+    size_t phase_op0 = 0;
+    auto classical_kind = [&](const Op &o) {
+        double d[4];
+        return o.kind == CX || o.kind == CZ || o.kind == CP || diag_of(o, d);
+    };
     for (size_t i = 0; i < G.ops.size(); ++i) {
         if (phases.empty() || needs_switch(i, regset)) {
+            if (!phases.empty() && !no_backup) {
+                size_t k = i;
+                while (k > phase_op0 && classical_kind(G.ops[k - 1].op)) --k;
+                const Op &oi = G.ops[i].op;
+                if (k > phase_op0 + 1 && G.ops[k - 1].op.kind == H && classical_kind(oi)) {
+                    const uint32_t tq = G.ops[k - 1].op.q0;
+                    size_t target = k - 1, m = k - 1;
+                    while (m > 0 && classical_kind(G.ops[m - 1].op)) --m;
+                    // inside the first run of a core (not the tail after its second H) and op i
+                    // still acts on the core's target
+                    const bool tail = m > 0 && G.ops[m - 1].op.kind == H && G.ops[m - 1].op.q0 == tq;
+                    const bool on_t = oi.q0 == tq || (two_qubit(oi.kind) && oi.q1 == tq);
+                    if (!tail && on_t && rec_at[target] != SIZE_MAX) {
+                        recs.resize(rec_at[target]);
+                        prm.resize(prm_at[target]);
+                        i = target;
+                    }
+                }
+            }
+            phase_op0 = i;
             if (!phases.empty()) phases.back().g1 = (uint16_t)recs.size();
             rs = lookahead(i, regset);
             regset = 0;
@@ -1187,6 +1218,8 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
             }
             phases.push_back(make_phase(rs, (uint16_t)recs.size()));
         }
+        rec_at[i] = recs.size();
+        prm_at[i] = prm.size();
         {
             size_t fe = i;
             uint32_t fmask = 0, fxor = 0;
@@ -1721,17 +1754,17 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 static const bool trace = getenv("TUSQ_TRACE_LAUNCHES") != nullptr;
                 char tag[160] = "";
                 if (trace) {
-                    int cnt[8] = {0};   // H, DK, CX/CX2, D1/D2, XPOSE, X/Y, T*, other
+                    int cnt[9] = {0};   // H, DK, CX/CX2, D1/D2, XPOSE, X/Y, T*, other, CU
                     for (uint32_t i = 0; i < P.ngate; ++i) {
                         const uint16_t c = P.g[i].code;
                         int k = c < C_U ? 0 : (c >= C_DK && c < C_CX2) ? 1 : ((c >= C_CX && c < C_CPH) || (c >= C_CX2 && c < C_CU)) ? 2
                                 : (c >= C_D1 && c < C_CX) ? 3 : c == C_XPOSE ? 4 : (c >= C_X && c < C_D1) ? 5
-                                : (c >= C_TX && c <= C_TPH) ? 6 : 7;
+                                : (c >= C_TX && c <= C_TPH) ? 6 : (c >= C_CU && c < C_N) ? 8 : 7;
                         cnt[k]++;
                     }
-                    snprintf(tag, sizeof(tag), "ops %zu recs %u ph %u init %d tile %#llx H%d DK%d CX%d D%d XP%d XY%d T%d O%d",
+                    snprintf(tag, sizeof(tag), "ops %zu recs %u ph %u init %d tile %#llx H%d DK%d CX%d D%d XP%d XY%d T%d O%d CU%d",
                              G.ops.size(), P.ngate, P.nphase, pending_init ? 1 : 0, (unsigned long long)B.tile, cnt[0],
-                             cnt[1], cnt[2], cnt[3], cnt[4], cnt[5], cnt[6], cnt[7]);
+                             cnt[1], cnt[2], cnt[3], cnt[4], cnt[5], cnt[6], cnt[7], cnt[8]);
                 }
                 ctx.timer->end(ctx.st, bytes, tag);
             }

@@ -65,6 +65,19 @@ def main():
     _, ops = W.adder(14)
     grp = [g for g in ops if g[0] != W.X][4 * 17: 8 * 17]
     rec(f"K5 fused ({len(grp)} gates)", 2 * N * s, timeit(lambda: T.apply_ops(st, n, prec, grp, 0, stream)))
+    # K5 cost anatomy: the bare sweep, register work without / with one transpose
+    variants = {
+        "K5 sweep (1 diagonal)": [W.op(W.T, 5)],
+        "K5 10 H, 1 phase": [W.op(W.H, q) for q in (3, 4, 5, 6, 7)] * 2,
+        "K5 9 H, 2 phases": [W.op(W.H, q) for q in (3, 4, 5, 6, 7, 8, 9, 10, 11)],
+        "K5 15 H, 3 phases": [W.op(W.H, q) for q in (3, 4, 5, 6, 7, 8, 9, 10, 11, 3, 4, 5, 6, 7, 8)],
+        "K5 8 DK (T/CX runs), 1 phase": [g for q in (3, 5) for g in
+                                         (W.op(W.CX, q, q + 1), W.op(W.T, q + 1), W.op(W.CX, q, q + 1),
+                                          W.op(W.TDG, q))] * 4,
+        "K5 4 Toffoli (CU records)": [g for g in W.adder(14)[1] if g[0] != W.X][4 * 17 + 2: 4 * 17 + 17],
+    }
+    for name, g in variants.items():
+        rec(name, 2 * N * s, timeit(lambda: T.apply_ops(st, n, prec, g, 0, stream)))
     rec("K7 init", N * s, timeit(lambda: T.init_basis(st, n, prec, 5, 1.0, 0.0, stream)))
     out = torch.zeros(8, dtype=torch.int64, device="cuda")
     rec("K6 sample (block sums + scan + 8 draws)", N * s, timeit(lambda: T.sample(st, n, prec, 8, 1, 0, out, stream)))
