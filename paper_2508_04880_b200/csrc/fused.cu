@@ -93,10 +93,6 @@ struct Phase {
     uint16_t so[NR];      // entering this phase: tile-local index read into register r
     uint16_t so_out[NR];  // leaving this phase: tile-local index register r is written to
                           // (they differ when register permutations are absorbed, host-computed)
-    // split transposes (half-tile buffer): the entering / leaving transpose's split bit s removed
-    // from so / so_out, and bit r = bit s of so[r] / so_out[r]
-    uint16_t soc[NR], so_outc[NR];
-    uint32_t hm_in, hm_out;
 };
 
 struct GRec {
@@ -536,8 +532,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
 {
     using V = typename CV<R>::T;
     extern __shared__ __align__(16) unsigned char smraw[];
-    V *sm = reinterpret_cast<V *>(smraw);              // tile staging (prefetch) buffer, 4096
-    V *sx = sm + (1 << TB);                              // split-transpose buffer, 2048
+    V *sm = reinterpret_cast<V *>(smraw);
     __shared__ double red[NT / 32];
     const uint32_t tid = threadIdx.x;
     const bool init = P.flags & F_INIT;
@@ -609,42 +604,6 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
             g._pad = 0;
             if (g.code != C_XPOSE) {
                 apply_gate<V, R>(a, g, P.prm, lbase);
-            } else if (g.pi != 0xFFFFu) {
-                // split transpose through the half-tile buffer: the slots whose (swizzled) index has
-                // bit s = h move in pass h -- the host picked s so that a register slot has the same
-                // pass in both layouts (no slot is overwritten before it is written out), and the
-                // staging buffer stays free for the next tile's prefetch
-                const Phase &prv = P.ph[ph];
-                const Phase &cur = P.ph[g.a];
-                ph = g.a;
-                const uint32_t sb = g.pi;
-                const uint32_t lm = (1u << sb) - 1u;
-                uint32_t ta = 0, tb = 0;
-#pragma unroll
-                for (int j = 0; j < NTB; ++j) {
-                    ta |= ((tid >> j) & 1u) << prv.tl[j];
-                    tb |= ((tid >> j) & 1u) << cur.tl[j];
-                }
-                ta = swz(ta);
-                tb = swz(tb);
-                const uint32_t th = (ta >> sb) & 1u;
-                const uint32_t ca = (ta & lm) | ((ta >> 1) & ~lm), cb = (tb & lm) | ((tb >> 1) & ~lm);
-                const uint32_t hmo = prv.hm_out, hmi = cur.hm_in;
-                const bool bar = !(g.b & 1);
-#pragma unroll
-                for (uint32_t h = 0; h < 2; ++h) {
-                    if (bar) __syncthreads();
-#pragma unroll
-                    for (int r = 0; r < NR; ++r)
-                        if ((((hmo >> r) & 1u) ^ th) == h) sx[ca ^ prv.so_outc[r]] = a[r];
-                    if (bar) __syncthreads();
-#pragma unroll
-                    for (int r = 0; r < NR; ++r)
-                        if ((((hmi >> r) & 1u) ^ th) == h) a[r] = sx[cb ^ cur.soc[r]];
-                }
-                lbase = base;
-#pragma unroll
-                for (int j = 0; j < NTB; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[cur.tl[j]];
             } else {
                 // transpose registers from the current layout to phase g.a through shared memory
                 const Phase &prv = P.ph[ph];
@@ -1613,43 +1572,6 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
             cur = r.a;
         }
     }
-    // Split bits for the transposes: s (>= 3, so the swizzle leaves it alone) such that every
-    // register slot (thread, r) has the same bit s in the leaving and the entering layout; then the
-    // transpose runs as two half-tile passes through the 2048-slot buffer.  Without one, the
-    // transpose uses the staging buffer (and the next tile's prefetch waits for it).
-    {
-        static const bool no_split = getenv("TUSQ_NO_SPLIT") != nullptr;
-        auto compress = [](uint32_t x, uint32_t sb) { return (x & ((1u << sb) - 1)) | ((x >> 1) & ~((1u << sb) - 1)); };
-        uint32_t cur = 0;
-        for (auto &r : recs) {
-            if (r.code != C_XPOSE) continue;
-            Phase &A = phases[cur], &Bp = phases[r.a];
-            cur = r.a;
-            r.pi = 0xFFFFu;
-            if (no_split) continue;
-            for (int sb = TB - 1; sb >= 3; --sb) {
-                int pa = -1, pb = -1;
-                for (int j = 0; j < NTB; ++j) {
-                    if (A.tl[j] == sb) pa = j;
-                    if (Bp.tl[j] == sb) pb = j;
-                }
-                if (pa != pb) continue;
-                bool ok = true;
-                for (int q = 0; q < NR && ok; ++q) ok = ((A.so_out[q] >> sb) & 1) == ((Bp.so[q] >> sb) & 1);
-                if (!ok) continue;
-                r.pi = (uint16_t)sb;
-                A.hm_out = 0;
-                Bp.hm_in = 0;
-                for (int q = 0; q < NR; ++q) {
-                    A.so_outc[q] = (uint16_t)compress(A.so_out[q], sb);
-                    Bp.soc[q] = (uint16_t)compress(Bp.so[q], sb);
-                    A.hm_out |= ((A.so_out[q] >> sb) & 1u) << q;
-                    Bp.hm_in |= ((Bp.so[q] >> sb) & 1u) << q;
-                }
-                break;
-            }
-        }
-    }
     static const bool dbg = getenv("TUSQ_DEBUG_PLAN") != nullptr;
     static const bool sigs = getenv("TUSQ_DEBUG_SIGS") != nullptr;
     if (sigs) {
@@ -1671,9 +1593,6 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                     for (int e = 0; e < (2 << __builtin_popcount(r.code - C_DK)); ++e)
                         fprintf(stderr, " %.3f", prm[r.pi + e]);
                 }
-            fprintf(stderr, "\n  split:");
-            for (auto &r : recs)
-                if (r.code == C_XPOSE) fprintf(stderr, " %d", r.pi == 0xFFFFu ? -1 : (int)r.pi);
             fprintf(stderr, "\n  phases:");
             for (auto &ph : phases) {
                 fprintf(stderr, " [g%u-%u regs", ph.g0, ph.g1);
@@ -1693,7 +1612,7 @@ static int blocks_per_sm(int prec)
     static int occ[2] = {0, 0};
     int &o = occ[prec == 128 ? 1 : 0];
     if (!o) {
-        size_t smem = (size_t)(3 << (TB - 1)) * (prec == 128 ? 16 : 8);
+        size_t smem = (size_t)(1 << TB) * (prec == 128 ? 16 : 8);
         if (prec == 128) {
             cudaFuncSetAttribute(k_fused<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused<double>, NT, smem);
@@ -1799,7 +1718,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             }
             P.last_xpose = 0xFFFFu;
             for (uint32_t i = 0; i < P.ngate; ++i)
-                if (P.g[i].code == C_XPOSE && P.g[i].pi == 0xFFFFu) P.last_xpose = (uint16_t)i;
+                if (P.g[i].code == C_XPOSE) P.last_xpose = (uint16_t)i;
         }
         P.ntiles = 1ull << (n_ - TB);
         P.flags = 0;
@@ -1825,7 +1744,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         if (!ctx.dry) {
             int bps = blocks_per_sm(prec_);
             uint64_t grid = std::min<uint64_t>(P.ntiles, (uint64_t)device_sm_count() * bps);
-            size_t smem = (size_t)(3 << (TB - 1)) * (prec_ == 128 ? 16 : 8);
+            size_t smem = (size_t)(1 << TB) * (prec_ == 128 ? 16 : 8);
             if (ctx.timer) ctx.timer->begin(ctx.st);
             if (prec_ == 128)
                 k_fused<double><<<(unsigned)grid, NT, smem, ctx.st>>>((double2 *)ctx.psi, P, d_sums);
