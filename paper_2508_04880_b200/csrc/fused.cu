@@ -822,6 +822,8 @@ FusedPlanner::FusedPlanner(uint32_t n, int prec, uint32_t tile_bits)
     (void)tile_bits;
 }
 
+static bool diag_of(const Op &o, double d[4]);
+
 // ---- group formation (greedy over the op stream) --------------------------------------
 static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
 {
@@ -860,9 +862,31 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
         g = Group();
         touched = 0;
     };
-    for (const Op &o : ops) {
+    // a Toffoli core H(t) [classical run] H(t) starting at op i: the qubits it touches (0: none)
+    static const bool no_core_groups = getenv("TUSQ_NO_CORE_GROUPS") != nullptr;
+    auto core_qubits = [&](size_t i) -> uint64_t {
+        const Op &h = ops[i];
+        if (no_core_groups || h.kind != H) return 0;
+        uint64_t m = bit(h.q0);
+        double d[4];
+        for (size_t j = i + 1; j < ops.size(); ++j) {
+            const Op &o = ops[j];
+            if (o.kind == H && o.q0 == h.q0) return j > i + 1 ? m : 0;
+            if (!(o.kind == CX || o.kind == CZ || o.kind == CP || diag_of(o, d))) return 0;
+            m |= op_qubits(o);
+        }
+        return 0;
+    };
+    for (size_t oi = 0; oi < ops.size(); ++oi) {
+        const Op &o = ops[oi];
         if (o.kind == I) continue;
         const uint64_t qm = op_qubits(o);
+        // keep a Toffoli core in one group (it folds into one controlled-2x2 record): close the
+        // group before the core's first H when the core's qubits would not fit
+        if (!g.ops.empty()) {
+            const uint64_t cq = core_qubits(oi);
+            if (cq && popc_hi(g.tilemask | cq) > TB - 3) close();
+        }
         // requirements of this op on the group's tile set
         const bool xy = (o.kind == X || o.kind == Y);
         uint64_t need = 0;
