@@ -71,6 +71,7 @@ def main():
         "K5 10 H, 1 phase": [W.op(W.H, q) for q in (3, 4, 5, 6, 7)] * 2,
         "K5 9 H, 2 phases": [W.op(W.H, q) for q in (3, 4, 5, 6, 7, 8, 9, 10, 11)],
         "K5 15 H, 3 phases": [W.op(W.H, q) for q in (3, 4, 5, 6, 7, 8, 9, 10, 11, 3, 4, 5, 6, 7, 8)],
+        "K5 20 H, 4 phases": [W.op(W.H, q) for q in (3, 4, 5, 6, 7, 8, 9, 10, 11, 3, 4, 5, 6, 7, 8, 9, 10, 11, 3, 4)],
         "K5 8 DK (T/CX runs), 1 phase": [g for q in (3, 5) for g in
                                          (W.op(W.CX, q, q + 1), W.op(W.T, q + 1), W.op(W.CX, q, q + 1),
                                           W.op(W.TDG, q))] * 4,
