@@ -72,13 +72,32 @@ def main():
         "K5 9 H, 2 phases": [W.op(W.H, q) for q in (3, 4, 5, 6, 7, 8, 9, 10, 11)],
         "K5 15 H, 3 phases": [W.op(W.H, q) for q in (3, 4, 5, 6, 7, 8, 9, 10, 11, 3, 4, 5, 6, 7, 8)],
         "K5 20 H, 4 phases": [W.op(W.H, q) for q in (3, 4, 5, 6, 7, 8, 9, 10, 11, 3, 4, 5, 6, 7, 8, 9, 10, 11, 3, 4)],
+        "K5 5 H on 12-16 (tile span 2^17)": [W.op(W.H, q) for q in (12, 13, 14, 15, 16)],
+        "K5 5 H on 20-24 (tile span 2^25)": [W.op(W.H, q) for q in (20, 21, 22, 23, 24)],
+        "K5 5 H on 25-29 (tile span 2^30)": [W.op(W.H, q) for q in (25, 26, 27, 28, 29)],
         "K5 8 DK (T/CX runs), 1 phase": [g for q in (3, 5) for g in
                                          (W.op(W.CX, q, q + 1), W.op(W.T, q + 1), W.op(W.CX, q, q + 1),
                                           W.op(W.TDG, q))] * 4,
         "K5 4 Toffoli (CU records)": [g for g in W.adder(14)[1] if g[0] != W.X][4 * 17 + 2: 4 * 17 + 17],
     }
+    gx = [g for g in W.adder(14)[1] if g[0] != W.X]
+    for k in (8, 9, 10):
+        variants[f"K5 4 MAJ on qubits {2 * k}-{2 * k + 8}"] = gx[k * 17:(k + 4) * 17]
     for name, g in variants.items():
         rec(name, 2 * N * s, timeit(lambda: T.apply_ops(st, n, prec, g, 0, stream)))
+    # the same groups launched alternately (as in a replay): per-launch times
+    ga, gb = gx[4 * 17:8 * 17], gx[9 * 17:13 * 17]
+    ta, tb = [], []
+    for it in range(6):
+        for g, lst in ((ga, ta), (gb, tb)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            T.apply_ops(st, n, prec, g, 0, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            lst.append(e0.elapsed_time(e1) / 1e3)
+    rec("K5 4 MAJ 8-16 alternating", 2 * N * s, sorted(ta)[len(ta) // 2])
+    rec("K5 4 MAJ 18-26 alternating", 2 * N * s, sorted(tb)[len(tb) // 2])
     rec("K7 init", N * s, timeit(lambda: T.init_basis(st, n, prec, 5, 1.0, 0.0, stream)))
     out = torch.zeros(8, dtype=torch.int64, device="cuda")
     rec("K6 sample (block sums + scan + 8 draws)", N * s, timeit(lambda: T.sample(st, n, prec, 8, 1, 0, out, stream)))
