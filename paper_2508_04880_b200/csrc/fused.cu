@@ -1442,7 +1442,7 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         recs.swap(m);
     }
     // Tunables (environment, for measurement): TUSQ_SPLIT_MIN (>= 2 enables phase splits after
-    // permutation runs), TUSQ_STORE_XPOSE=1 (coalescing transpose before the store).
+    // permutation runs), TUSQ_STORE_XPOSE=0 (no coalescing transpose before the store).
     static const size_t split_min = getenv("TUSQ_SPLIT_MIN") ? (size_t)atoi(getenv("TUSQ_SPLIT_MIN")) : 1000;
     // store transpose: default on (measured: the UMA group that ends on qubits 0-4 in registers
     // writes 2x the L2 sectors; 13.9 -> 12.4 ms per launch with one more transpose)
