@@ -118,6 +118,18 @@ def workload_desc(cfg) -> str:
             + (f" p_meas={nz.p_meas}" if nz.p_meas else "") + f", {cfg.shots} shots, seed {cfg.seed}, alpha 1/100, beta 100")
 
 
+def ncu_traffic(prec, no_fuse):
+    """DRAM bytes per k_fused launch from the committed ncu --set full capture of this bench (c128)."""
+    path = os.path.join(ROOT, "profiles", "r1_ncu_k_fused_in_bench.json")
+    if no_fuse or prec != 128 or not os.path.exists(path):
+        return None
+    try:
+        caps = json.load(open(path))["full_capture"]
+        return caps[0].get("dram_traffic_bytes")
+    except (OSError, ValueError, KeyError, IndexError):
+        return None
+
+
 def run_reference(args, rank, world):
     """The CPU oracle (test infrastructure) timed on the host cores on this workload."""
     if rank != 0:
@@ -262,7 +274,9 @@ def main():
                    "l2": f"state {state.numel() * state.element_size() / 2**30:.0f} GiB >> 126 MB L2 (no flush needed)",
                    "fused": not args.no_fuse, "parallelism": f"replica x{world}, contiguous DFS leaf ranges"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": ncu_traffic(prec, args.no_fuse),
+                     "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one k_fused launch of this "
+                                       "bench under ncu --set full (profiles/r1_ncu_k_fused_in_bench.json)",
                      "kernel": "k_fused (K5)" if not args.no_fuse else "K1-K4",
                      "launches_timed": gk_n, "bytes_per_launch": gk_b / max(gk_n, 1),
                      "avg_launch_ms": gk_s / max(gk_n, 1) * 1e3, "peak_source": peak_src,

@@ -1364,7 +1364,18 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         for (size_t j = 0; j < recs.size(); ++j) {
             newidx[j] = (uint16_t)m.size();
             const uint16_t c0 = recs[j].code;
-            if (!no_cu && j + 2 < recs.size() && c0 < C_H + RB && recs[j + 2].code == c0 && recs[j + 1].code >= C_DK &&
+            // X records between the table and the second H (a Pauli error folded into the core):
+            // H X_S D H = Z_p^[p in S] X_S' (H D H), S' = S \ {p} -- the Z joins the blocks, the
+            // X's follow the record (and conjugate a trailing control diagonal)
+            size_t k2 = j + 2;
+            uint32_t xs = 0;
+            if (j + 1 < recs.size() && recs[j + 1].code >= C_DK && recs[j + 1].code < C_DK + NR)
+                while (k2 < recs.size() && recs[k2].code >= C_X && recs[k2].code < C_X + RB &&
+                       (((recs[j + 1].code - C_DK) >> (recs[k2].code - C_X)) & 1)) {
+                    xs ^= 1u << (recs[k2].code - C_X);
+                    ++k2;
+                }
+            if (!no_cu && k2 < recs.size() && c0 < C_H + RB && recs[k2].code == c0 && recs[j + 1].code >= C_DK &&
                 recs[j + 1].code < C_DK + NR) {
                 const int p = c0 - C_H, mask = recs[j + 1].code - C_DK;
                 int jj = -1;
@@ -1372,14 +1383,16 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                     if (hdh_mask(p, q) == mask) jj = q;
                 if (jj >= 0 && code_ok(C_CU + 6 * p + jj)) {
                     const int cm = mask & ~(1 << p);
+                    const bool zp = (xs >> p) & 1u;
+                    const uint32_t xo = xs & ~(1u << p);
                     const double *t1 = &prm[recs[j + 1].pi];
                     // optional trailing diagonal on the controls
                     const double *t2 = nullptr;
                     int m2 = 0;
-                    if (j + 3 < recs.size() && recs[j + 3].code > C_DK && recs[j + 3].code < C_DK + NR &&
-                        ((recs[j + 3].code - C_DK) & ~cm) == 0) {
-                        m2 = recs[j + 3].code - C_DK;
-                        t2 = &prm[recs[j + 3].pi];
+                    if (k2 + 1 < recs.size() && recs[k2 + 1].code > C_DK && recs[k2 + 1].code < C_DK + NR &&
+                        ((recs[k2 + 1].code - C_DK) & ~cm) == 0) {
+                        m2 = recs[k2 + 1].code - C_DK;
+                        t2 = &prm[recs[k2 + 1].pi];
                     }
                     auto pextm = [](uint32_t x, uint32_t mk) {
                         uint32_t o = 0, k = 0;
@@ -1397,12 +1410,14 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                         const double d0r = t1[2 * pextm(x0, mask)], d0i = t1[2 * pextm(x0, mask) + 1];
                         const double d1r = t1[2 * pextm(x1, mask)], d1i = t1[2 * pextm(x1, mask) + 1];
                         double fr = 1.0, fi = 0.0;
-                        if (t2) { fr = t2[2 * pextm(x0, m2)]; fi = t2[2 * pextm(x0, m2) + 1]; }
+                        if (t2) { fr = t2[2 * pextm(x0 ^ xo, m2)]; fi = t2[2 * pextm(x0 ^ xo, m2) + 1]; }
                         // (1/2) [[d0 + d1, d0 - d1], [d0 - d1, d0 + d1]] * f   (= H diag(d0, d1) H, then f)
                         const double sr = 0.5 * (d0r + d1r), si = 0.5 * (d0i + d1i);
                         const double ar = 0.5 * (d0r - d1r), ai = 0.5 * (d0i - d1i);
                         double e[8] = {sr * fr - si * fi, sr * fi + si * fr, ar * fr - ai * fi, ar * fi + ai * fr,
                                        ar * fr - ai * fi, ar * fi + ai * fr, sr * fr - si * fi, sr * fi + si * fr};
+                        if (zp)
+                            for (int q = 4; q < 8; ++q) e[q] = -e[q];   // Z on t after the block
                         // snap to the exact values the algebra gives (errors <= a few ulp)
                         for (double &v : e) {
                             if (fabs(v) < 1e-15) v = 0.0;
@@ -1428,10 +1443,17 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                     r.pi = (uint16_t)prm.size();
                     prm.insert(prm.end(), blk.begin(), blk.end());
                     m.push_back(r);
+                    for (int b = 0; b < RB; ++b)
+                        if ((xo >> b) & 1u) {
+                            GRec xr;
+                            memset(&xr, 0, sizeof(xr));
+                            xr.code = (uint16_t)(C_X + b);
+                            m.push_back(xr);
+                        }
                     B.h_absorbed += 2;
-                    const size_t used = t2 ? 4 : 3;
-                    for (size_t q = 1; q < used; ++q) newidx[j + q] = (uint16_t)m.size();
-                    j += used - 1;
+                    const size_t last = t2 ? k2 + 1 : k2;
+                    for (size_t q = j + 1; q <= last; ++q) newidx[q] = (uint16_t)m.size();
+                    j = last;
                     continue;
                 }
             }
