@@ -115,6 +115,9 @@ struct Params {
     uint32_t rx;                  // register bits where xm_load is set (folded into gl, kept 0)
     uint16_t mloc;                // tile-local bits of xm_load (applied when copying to shared memory)
     uint16_t last_xpose;          // record index of the last transpose (0xFFFF: none)
+    uint16_t st_pair;             // 0, or 1 + (register bit k carrying qubit 0 in the last layout)
+                                  // + 8 * inv: registers r, r ^ 2^k are adjacent amplitudes ->
+                                  // one 2x-wide store (inv: the one with bit k set is the even one)
     uint64_t regm_load;           // global mask of the phase-0 register qubits
     uint64_t gj[NR];              // global offset of tile-local index (j << NTB) (copy slots)
     uint16_t sj[NR];              // swz(j << NTB): swizzled shared-memory part of copy slot j
@@ -526,6 +529,31 @@ __device__ __forceinline__ void prefetch_tile(V *sm, const V *psi, uint64_t T, c
     cp_async_commit();
 }
 
+// 32-byte (c128) / 16-byte (c64) streaming store of two adjacent amplitudes
+__device__ __forceinline__ void st_pair(double2 *q, const double2 &lo, const double2 &hi)
+{
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(q), "d"(lo.x), "d"(lo.y), "d"(hi.x), "d"(hi.y)
+                 : "memory");
+}
+__device__ __forceinline__ void st_pair(float2 *q, const float2 &lo, const float2 &hi)
+{
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(q), "f"(lo.x), "f"(lo.y), "f"(hi.x), "f"(hi.y)
+                 : "memory");
+}
+// store with qubit 0 on register bit K: every lane writes whole 32-byte sectors (a plain 16-byte
+// store per register would leave each sector half-written per instruction: 2x L2 sectors)
+template <int K, typename V>
+__device__ __forceinline__ void store_pairs(V *q0, const V (&a)[NR], const Params &P, bool inv)
+{
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+        if (!(r & (1 << K))) {
+            const int r1 = r | (1 << K);
+            if (inv) st_pair(q0 + P.gs[r1], a[r1], a[r]);
+            else st_pair(q0 + P.gs[r], a[r], a[r1]);
+        }
+}
+
 template <typename R>
 __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ psi, const __grid_constant__ Params P,
                                              double *__restrict__ sums)
@@ -661,8 +689,19 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
         }
         // xm_store has no tile bits: register offsets are additive
         V *q0 = psi + ((base | gthr) ^ P.xm_store);
+        if (P.st_pair) {
+            const bool inv = P.st_pair & 8;
+            switch ((P.st_pair & 7) - 1) {
+            case 0: store_pairs<0>(q0, a, P, inv); break;
+            case 1: store_pairs<1>(q0, a, P, inv); break;
+            case 2: store_pairs<2>(q0, a, P, inv); break;
+            case 3: store_pairs<3>(q0, a, P, inv); break;
+            default: if constexpr (RB > 4) store_pairs<4>(q0, a, P, inv); break;
+            }
+        } else {
 #pragma unroll
-        for (int r = 0; r < NR; ++r) __stcs(q0 + P.gs[r], a[r]);
+            for (int r = 0; r < NR; ++r) __stcs(q0 + P.gs[r], a[r]);
+        }
         if (P.flags & F_SUMS) {
             double s = 0.0;
 #pragma unroll
@@ -1464,11 +1503,12 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         recs.swap(m);
     }
     // Tunables (environment, for measurement): TUSQ_SPLIT_MIN (>= 2 enables phase splits after
-    // permutation runs), TUSQ_STORE_XPOSE=0 (no coalescing transpose before the store).
+    // permutation runs), TUSQ_STORE_XPOSE=1 (coalescing transpose before the store).
     static const size_t split_min = getenv("TUSQ_SPLIT_MIN") ? (size_t)atoi(getenv("TUSQ_SPLIT_MIN")) : 1000;
-    // store transpose: default on (measured: the UMA group that ends on qubits 0-4 in registers
-    // writes 2x the L2 sectors; 13.9 -> 12.4 ms per launch with one more transpose)
-    static const bool store_xpose = !(getenv("TUSQ_STORE_XPOSE") && getenv("TUSQ_STORE_XPOSE")[0] == '0');
+    // store transpose (opt-in): superseded by paired 32-byte stores when qubit 0 ends in a register
+    // (the UMA group that ends on qubits 0-4 in registers wrote 2x the L2 sectors: 13.9 ms; with a
+    // store transpose 12.4 ms)
+    static const bool store_xpose = getenv("TUSQ_STORE_XPOSE") && getenv("TUSQ_STORE_XPOSE")[0] == '1';
     // Split a phase right after an interior run of >= 2 register-permutation records (e.g. the
     // two trailing CXs of every Cuccaro UMA): the run then ends its phase and is absorbed into the
     // transpose that follows (same register set), trading ~2 swap passes for one transpose.
@@ -1753,6 +1793,17 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 P.gs[r] = goff(l, B.pout_last[r]);
             }
             P.rx = 0;
+            // paired stores when qubit 0 is a register bit of the last layout
+            P.st_pair = 0;
+            for (int k = 0; k < RB && !P.st_pair; ++k) {
+                const bool inv = P.gs[0] & 1;
+                bool ok = true;
+                for (int r = 0; r < NR && ok; ++r)
+                    ok = (P.gs[r ^ (1 << k)] == (P.gs[r] ^ 1ull)) && (((P.gs[r] & 1) != 0) == (inv ^ ((r >> k) & 1)));
+                if (ok) P.st_pair = (uint16_t)(1 + k + (inv ? 8 : 0));
+            }
+            static const bool no_pair = getenv("TUSQ_NO_PAIR_STORE") != nullptr;
+            if (no_pair) P.st_pair = 0;
             // shared-memory staging of loads: copy-slot offsets, tile-local XOR mask, last transpose
             P.mloc = 0;
             for (int b = 0; b < TB; ++b)
