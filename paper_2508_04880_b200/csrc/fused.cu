@@ -115,9 +115,9 @@ struct Params {
     uint32_t rx;                  // register bits where xm_load is set (folded into gl, kept 0)
     uint16_t mloc;                // tile-local bits of xm_load (applied when copying to shared memory)
     uint16_t last_xpose;          // record index of the last transpose (0xFFFF: none)
-    uint16_t st_pair;             // 0, or 1 + (register bit k carrying qubit 0 in the last layout)
-                                  // + 8 * inv: registers r, r ^ 2^k are adjacent amplitudes ->
-                                  // one 2x-wide store (inv: the one with bit k set is the even one)
+    uint16_t st_pair;             // 0, or v: registers r, r ^ v hold adjacent amplitudes in the last
+                                  // layout -> one 2x-wide store per pair
+    uint32_t st_odd;              // bit r: register r holds the odd one of its pair
     uint64_t regm_load;           // global mask of the phase-0 register qubits
     uint64_t gj[NR];              // global offset of tile-local index (j << NTB) (copy slots)
     uint16_t sj[NR];              // swz(j << NTB): swizzled shared-memory part of copy slot j
@@ -542,14 +542,17 @@ __device__ __forceinline__ void st_pair(float2 *q, const float2 &lo, const float
 }
 // store with qubit 0 on register bit K: every lane writes whole 32-byte sectors (a plain 16-byte
 // store per register would leave each sector half-written per instruction: 2x L2 sectors)
-template <int K, typename V>
-__device__ __forceinline__ void store_pairs(V *q0, const V (&a)[NR], const Params &P, bool inv)
+template <int PV, typename V>
+__device__ __forceinline__ void store_pairs(V *q0, const V (&a)[NR], const Params &P)
 {
+    // PV: the register-index difference of the two registers holding adjacent amplitudes
+    constexpr int HB = 31 - __builtin_clz(PV);
+    const uint32_t odd = P.st_odd;
 #pragma unroll
     for (int r = 0; r < NR; ++r)
-        if (!(r & (1 << K))) {
-            const int r1 = r | (1 << K);
-            if (inv) st_pair(q0 + P.gs[r1], a[r1], a[r]);
+        if (!(r & (1 << HB))) {
+            const int r1 = r ^ PV;
+            if ((odd >> r) & 1u) st_pair(q0 + P.gs[r1], a[r1], a[r]);
             else st_pair(q0 + P.gs[r], a[r], a[r1]);
         }
 }
@@ -690,13 +693,14 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
         // xm_store has no tile bits: register offsets are additive
         V *q0 = psi + ((base | gthr) ^ P.xm_store);
         if (P.st_pair) {
-            const bool inv = P.st_pair & 8;
-            switch ((P.st_pair & 7) - 1) {
-            case 0: store_pairs<0>(q0, a, P, inv); break;
-            case 1: store_pairs<1>(q0, a, P, inv); break;
-            case 2: store_pairs<2>(q0, a, P, inv); break;
-            case 3: store_pairs<3>(q0, a, P, inv); break;
-            default: if constexpr (RB > 4) store_pairs<4>(q0, a, P, inv); break;
+            switch (P.st_pair) {
+#define TQ_SP(v) case v: if constexpr (v < NR) store_pairs<v>(q0, a, P); break;
+                TQ_SP(1) TQ_SP(2) TQ_SP(3) TQ_SP(4) TQ_SP(5) TQ_SP(6) TQ_SP(7) TQ_SP(8) TQ_SP(9) TQ_SP(10)
+                TQ_SP(11) TQ_SP(12) TQ_SP(13) TQ_SP(14) TQ_SP(15) TQ_SP(16) TQ_SP(17) TQ_SP(18) TQ_SP(19)
+                TQ_SP(20) TQ_SP(21) TQ_SP(22) TQ_SP(23) TQ_SP(24) TQ_SP(25) TQ_SP(26) TQ_SP(27) TQ_SP(28)
+                TQ_SP(29) TQ_SP(30) TQ_SP(31)
+#undef TQ_SP
+            default: break;
             }
         } else {
 #pragma unroll
@@ -1795,15 +1799,22 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             P.rx = 0;
             // paired stores when qubit 0 is a register bit of the last layout
             P.st_pair = 0;
-            for (int k = 0; k < RB && !P.st_pair; ++k) {
-                const bool inv = P.gs[0] & 1;
+            P.st_odd = 0;
+            for (int v = 1; v < NR && !P.st_pair; ++v) {
                 bool ok = true;
-                for (int r = 0; r < NR && ok; ++r)
-                    ok = (P.gs[r ^ (1 << k)] == (P.gs[r] ^ 1ull)) && (((P.gs[r] & 1) != 0) == (inv ^ ((r >> k) & 1)));
-                if (ok) P.st_pair = (uint16_t)(1 + k + (inv ? 8 : 0));
+                for (int r = 0; r < NR && ok; ++r) ok = P.gs[r ^ v] == (P.gs[r] ^ 1ull);
+                if (ok) {
+                    P.st_pair = (uint16_t)v;
+                    for (int r = 0; r < NR; ++r) P.st_odd |= (uint32_t)(P.gs[r] & 1) << r;
+                }
             }
             static const bool no_pair = getenv("TUSQ_NO_PAIR_STORE") != nullptr;
             if (no_pair) P.st_pair = 0;
+            if (getenv("TUSQ_DEBUG_PLAN")) {
+                fprintf(stderr, "  st_pair %u gs:", P.st_pair);
+                for (int r = 0; r < NR; ++r) fprintf(stderr, " %llx", (unsigned long long)P.gs[r]);
+                fprintf(stderr, "\n");
+            }
             // shared-memory staging of loads: copy-slot offsets, tile-local XOR mask, last transpose
             P.mloc = 0;
             for (int b = 0; b < TB; ++b)
