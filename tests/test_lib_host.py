@@ -14,7 +14,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="session")
 def lib():
-    from paper_2508_04880_b200 import build
+    # build.py by path: the package import raises until libtusq.so exists
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_tusq_build", os.path.join(ROOT, "paper_2508_04880_b200", "build.py"))
+    build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(build)
     build.build()
     import paper_2508_04880_b200 as T
     return T
