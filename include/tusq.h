@@ -178,6 +178,9 @@ tusq_status tusq_sample(const void *d_state, uint32_t n_qubits, uint32_t precisi
  * the inverse circuit (inverse gates in reverse order); TUSQ_APPLY_UNFUSED forces one kernel per gate. */
 #define TUSQ_APPLY_INVERSE   0x1u
 #define TUSQ_APPLY_UNFUSED   0x2u
+/* TUSQ_APPLY_PLAN_ONLY: run the host planner only (no device access; d_state may be any non-NULL
+ * value); with TUSQ_DEBUG_PLAN=2 in the environment the K5 group plans are printed to stderr. */
+#define TUSQ_APPLY_PLAN_ONLY 0x4u
 tusq_status tusq_apply_ops(void *d_state, uint32_t n_qubits, uint32_t precision, const tusq_op *ops,
                            uint64_t n_ops, uint32_t flags, void *stream);
 

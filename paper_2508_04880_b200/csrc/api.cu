@@ -192,6 +192,7 @@ tusq_status tusq_apply_ops(void *d_state, uint32_t n, uint32_t precision, const 
     tusq_run_stats stats{};
     Ctx ctx;
     ctx.psi = d_state; ctx.n = n; ctx.prec = (int)precision; ctx.st = (cudaStream_t)stream; ctx.stats = &stats;
+    ctx.dry = (flags & TUSQ_APPLY_PLAN_ONLY) != 0;
     FusedPlanner planner(n, (int)precision, 0);
     try {
         if (!(flags & TUSQ_APPLY_UNFUSED) && planner.enabled()) {
@@ -203,7 +204,7 @@ tusq_status tusq_apply_ops(void *d_state, uint32_t n, uint32_t precision, const 
     } catch (const std::exception &e) {
         return fail(TUSQ_ERR_INTERNAL, e.what());
     }
-    TQ_CUDA(cudaGetLastError());
+    if (!ctx.dry) TQ_CUDA(cudaGetLastError());
     return TUSQ_OK;
 }
 

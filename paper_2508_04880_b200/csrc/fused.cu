@@ -42,6 +42,14 @@ constexpr int NR = 1 << RB;        // amplitudes per thread
 constexpr int NTB = TB - RB;       // thread bits (5 lane bits + warp bits)
 constexpr int NT = 1 << NTB;       // threads per CTA
 constexpr int MAXPH = 24;
+#ifndef TQ_NG
+#define TQ_NG 2
+#endif
+#ifndef TQ_NBUF
+#define TQ_NBUF 3
+#endif
+constexpr int NG = TQ_NG;      // tile groups (of NT threads) per CTA
+constexpr int NBUF = TQ_NBUF;  // tile buffers per CTA (shared memory)
 constexpr int MAXG = 400;
 constexpr int MAXP = 1600;
 
@@ -60,8 +68,9 @@ enum Code : uint16_t {
     C_DK = 91,    // +mask   a[r] *= tab[pext(r, mask)]  (2 * 2^popc(mask) params)
     C_CX2 = 123,  // +25c+5t1+t2 (t1 < t2): CX(c->t1) CX(c->t2) as ONE swap pass
     C_CU = 248,   // +6p+j   2x2 on bit p per pattern of the control pair j (Toffoli cores), 32 params
-    C_N = 278,    // number of gate codes
-    C_XPOSE = 278 // transpose registers to phase a
+    C_CCX = 278,  // +6p+j   Toffoli on register bits: swap bit p where both controls of pair j are 1
+    C_N = 308,    // number of gate codes
+    C_XPOSE = 308 // transpose registers to phase a
 };
 
 // the j-th (0..5) pair {u < v} of register bits other than p, as a mask (with p): the diagonal of a
@@ -119,10 +128,15 @@ struct Params {
                                   // layout -> one 2x-wide store per pair
     uint32_t st_odd;              // bit r: register r holds the odd one of its pair
     uint64_t regm_load;           // global mask of the phase-0 register qubits
+    uint64_t outer;               // mask of the outer (non-tile) qubits
+    uint64_t dstep;               // pdep(gridDim.x * NG, outer): next tile of the same group
+    uint64_t dissue[NG];          // pdep(T(j + NBUF) - T(j), outer) for a tile j of group g
+    // gj, gs, sj and the phases' so / so_out are BYTE offsets at launch (element offsets while
+    // the host plans): the kernel adds them to byte pointers with no index scaling
     uint64_t gj[NR];              // global offset of tile-local index (j << NTB) (copy slots)
     uint16_t sj[NR];              // swz(j << NTB): swizzled shared-memory part of copy slot j
     uint64_t gl[NR];              // phase 0: global element offset of register r (additive)
-    uint64_t gs[NR];              // last phase: global element offset of register r (additive)
+    uint64_t gs[NR];              // last phase: global offset of register r (additive)
     Phase ph[MAXPH];
     GRec g[MAXG];
     double prm[MAXP];
@@ -288,12 +302,14 @@ __device__ __forceinline__ void g_cx2(V (&a)[NR])
         if ((i & (1 << C)) && !(i & (1 << T1))) vswap(a[i], a[i ^ (1 << T1) ^ (1 << T2)]);
 }
 
-template <int C, int T, typename V>
+// CX(c -> t); with MASK, C is a mask of control bits (all must be 1: a Toffoli for two bits)
+template <int C, int T, typename V, bool MASK = false>
 __device__ __forceinline__ void g_cx(V (&a)[NR])
 {
+    constexpr int CM = MASK ? C : (1 << C);
 #pragma unroll
     for (int i = 0; i < NR; ++i)
-        if ((i & (1 << C)) && !(i & (1 << T))) vswap(a[i], a[i | (1 << T)]);
+        if ((i & CM) == CM && !(i & (1 << T))) vswap(a[i], a[i | (1 << T)]);
 }
 
 template <int A, int B, typename V, typename R>
@@ -402,6 +418,7 @@ __host__ __device__ constexpr bool code_ok(int C)
     if (C < C_TPH) return (C - C_TX) % 5 < RB;
     if (C == C_TPH) return true;
     if (C < C_CX2) return C - C_DK < NR;
+    if (C >= C_CCX) return hdh_mask((C - C_CCX) / 6, (C - C_CCX) % 6) < NR;
     if (C >= C_CU) return hdh_mask((C - C_CU) / 6, (C - C_CU) % 6) < NR;
     const int c = (C - C_CX2) / 25, t1 = (C - C_CX2) / 5 % 5, t2 = (C - C_CX2) % 5;
     return c < RB && t1 < RB && t2 < RB && t1 < t2 && c != t1 && c != t2;
@@ -441,6 +458,9 @@ __device__ __forceinline__ void gate_case(V (&a)[NR], const double *p, uint64_t 
 #pragma unroll
             for (int i = 0; i < NR; ++i) cmul_ip(a[i], fr, fi);
         }
+    } else if constexpr (C >= C_CCX) {
+        constexpr int pb = (C - C_CCX) / 6;
+        g_cx<(hdh_mask(pb, (C - C_CCX) % 6) & ~(1 << pb)), pb, V, true>(a);
     } else if constexpr (C >= C_CU) {
         constexpr int pb = (C - C_CU) / 6;
         g_cu<pb, hdh_mask(pb, (C - C_CU) % 6) & ~(1 << pb), V, R>(a, p, gb, ga);
@@ -469,11 +489,15 @@ template <typename V, typename R>
 __device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const double *prm, uint64_t lbase)
 {
     // fast paths for the two hottest classes (H and diagonal tables: ~2/3 of all records)
+    // ordered by frequency in Adder groups: Toffoli swaps, CX, diagonal tables, H, CU, rest
     const int c = g.code;
-    if (c < C_U) dispatch<0, C_U, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    if (c >= C_CCX) dispatch<C_CCX, C_N, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else if (c >= C_CX && c < C_CPH) dispatch<C_CX, C_CPH, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
     else if (c >= C_DK && c < C_DK + NR) dispatch<C_DK, C_DK + NR, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
-    else if (c < C_DK) dispatch<C_U, C_DK, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
-    else if (c >= C_CU) dispatch<C_CU, C_N, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else if (c < C_U) dispatch<0, C_U, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else if (c >= C_CU) dispatch<C_CU, C_CCX, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else if (c < C_CX) dispatch<C_U, C_CX, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else if (c < C_DK) dispatch<C_CPH, C_DK, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
     else dispatch<C_CX2, C_CU, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
 }
 
@@ -518,14 +542,15 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t T, const uint8_t (&qs)[TB
 // tile order: thread tid copies physical local indices p = tid + NT*j (coalesced: lanes 0-7 run
 // over qubits 0,1,2), to slot swz(p ^ mloc).
 template <typename V>
-__device__ __forceinline__ void prefetch_tile(V *sm, const V *psi, uint64_t T, const Params &P, uint64_t gt,
+__device__ __forceinline__ void prefetch_tile(V *sm, const V *psi, uint64_t tbase, const Params &P, uint64_t gt,
                                               uint32_t tid)
 {
-    const V *src = psi + (tile_base(T, P.qs) ^ P.xm_store) + gt;
+    // tbase: the tile's logical base (outer bits); all offsets below are in bytes
+    const char *src = reinterpret_cast<const char *>(psi + ((tbase ^ P.xm_store) + gt));
+    char *dst = reinterpret_cast<char *>(sm);
+    const uint32_t st = swz(tid ^ P.mloc) * (uint32_t)sizeof(V);
 #pragma unroll
-    const uint32_t st = swz(tid ^ P.mloc);
-#pragma unroll
-    for (int j = 0; j < NR; ++j) cp_async<sizeof(V)>(sm + (st ^ P.sj[j]), src + P.gj[j]);
+    for (int j = 0; j < NR; ++j) cp_async<sizeof(V)>(dst + (st ^ P.sj[j]), src + P.gj[j]);
     cp_async_commit();
 }
 
@@ -548,35 +573,108 @@ __device__ __forceinline__ void store_pairs(V *q0, const V (&a)[NR], const Param
     // PV: the register-index difference of the two registers holding adjacent amplitudes
     constexpr int HB = 31 - __builtin_clz(PV);
     const uint32_t odd = P.st_odd;
+    char *qb = reinterpret_cast<char *>(q0);
 #pragma unroll
     for (int r = 0; r < NR; ++r)
         if (!(r & (1 << HB))) {
             const int r1 = r ^ PV;
-            if ((odd >> r) & 1u) st_pair(q0 + P.gs[r1], a[r1], a[r]);
-            else st_pair(q0 + P.gs[r], a[r], a[r1]);
+            if ((odd >> r) & 1u) st_pair(reinterpret_cast<V *>(qb + P.gs[r1]), a[r1], a[r]);
+            else st_pair(reinterpret_cast<V *>(qb + P.gs[r]), a[r], a[r1]);
         }
 }
 
+// ---- tile pipeline: NG independent 128-thread tile groups per CTA share NBUF tile buffers.
+// Tile j of a CTA (j = 0, 1, 2, ...) is handled by group j % NG and lives in buffer j % NBUF from
+// its load until its last transpose.  At that point its group RELEASES the buffer by issuing the
+// load of tile j + NBUF (the other group's) into it; completion is tracked by an mbarrier
+// (cp.async.mbarrier.arrive.noinc), so the group that waits need not be the group that issued.
+// With NG = 2, NBUF = 3 every tile's load is issued about one tile period before it is needed,
+// whatever the position of the group's last transpose (before: one shared buffer per 128-thread
+// CTA, so the next load could only start after the last transpose).
+__device__ __forceinline__ void named_bar(uint32_t id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NT) : "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t *m, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(m)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *m)
+{
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(m))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t *m)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"((unsigned)__cvta_generic_to_shared(m))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(m)),
+                 "r"(parity)
+                 : "memory");
+}
+
+// tile index of this CTA's j-th tile
+__device__ __forceinline__ uint64_t cta_tile(uint64_t j)
+{
+    return (uint64_t)blockIdx.x * NG + (j % NG) + (j / NG) * ((uint64_t)gridDim.x * NG);
+}
+
+// Hand buffer j % NBUF over to tile j (issued by the group that held it): load tile j into it, or
+// (F_INIT: nothing to load) just arrive.  Called by all NT threads of the issuing group.
+template <typename V>
+__device__ __forceinline__ void issue_tile(V *smbase, uint64_t *mbar, const V *psi, uint64_t j, uint64_t tbase,
+                                           const Params &P, uint64_t gt, uint32_t tid, bool init)
+{
+    if (cta_tile(j) >= P.ntiles) return;
+    const int b = (int)(j % NBUF);
+    if (init) {
+        mbar_arrive(&mbar[b]);
+    } else {
+        prefetch_tile(smbase + (size_t)b * (1u << TB), psi, tbase, P, gt, tid);
+        mbar_arrive_cp_async(&mbar[b]);
+    }
+}
+
+// tile bases step in the deposited (outer-bit) domain: filling the holes with ones lets the
+// carries of an ordinary add run through them (pdep(x + y) = ((pdep x | ~m) + pdep y) & m)
+__device__ __forceinline__ uint64_t dep_add(uint64_t x, uint64_t dy, uint64_t m) { return ((x | ~m) + dy) & m; }
+
 template <typename R>
-__global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ psi, const __grid_constant__ Params P,
-                                             double *__restrict__ sums)
+__global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename CV<R>::T *__restrict__ psi,
+                                                      const __grid_constant__ Params P, double *__restrict__ sums)
 {
     using V = typename CV<R>::T;
     extern __shared__ __align__(16) unsigned char smraw[];
-    V *sm = reinterpret_cast<V *>(smraw);
-    __shared__ double red[NT / 32];
-    const uint32_t tid = threadIdx.x;
+    V *smbase = reinterpret_cast<V *>(smraw);
+    __shared__ uint64_t mbar[NBUF];
+    __shared__ double red[NG][NT / 32];
+    const uint32_t grp = threadIdx.x / NT;
+    const uint32_t tid = threadIdx.x % NT;
+    const uint32_t bar = 1 + grp;     // named barrier of this tile group (0 = __syncthreads)
     const bool init = P.flags & F_INIT;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NBUF; ++b) mbar_init(&mbar[b], NT);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
     // global offset of this thread's copy slot: tile-local bits 0..NTB-1 = tid (tile independent)
     uint64_t gt = 0;
 #pragma unroll
     for (int b = 0; b < NTB; ++b) gt |= (uint64_t)((tid >> b) & 1u) << P.qs[b];
-    if (!init && blockIdx.x < P.ntiles) prefetch_tile(sm, psi, blockIdx.x, P, gt, tid);
+    // the first NBUF tiles: tile j is issued by group j % NG
+    for (uint64_t j = grp; j < NBUF; j += NG) issue_tile(smbase, mbar, psi, j, tile_base(cta_tile(j), P.qs), P, gt, tid, init);
     V a[NR];
-    for (uint64_t T = blockIdx.x; T < P.ntiles; T += gridDim.x) {
-        // logical tile base: the tile index deposited into the outer (non-tile) qubit positions
-        const uint64_t base = tile_base(T, P.qs);
-        const uint64_t Tn = T + gridDim.x;
+    // logical tile base: the tile index deposited into the outer (non-tile) qubit positions
+    uint64_t base = tile_base(cta_tile(grp), P.qs);
+    const uint64_t dissue = P.dissue[grp];
+    for (uint64_t j = grp;; j += NG, base = dep_add(base, P.dstep, P.outer)) {
+        const uint64_t T = cta_tile(j);
+        if (T >= P.ntiles) break;
+        V *sm = smbase + (size_t)(j % NBUF) * (1u << TB);
+        char *smb = reinterpret_cast<char *>(sm);
 
         // ---- phase 0 layout: global offset of this thread's bits; register offsets come from
         // the parameter block (constant bank), added to one base pointer
@@ -584,8 +682,9 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
         {
             const Phase &p0 = P.ph[0];
 #pragma unroll
-            for (int j = 0; j < NTB; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[p0.tl[j]];
+            for (int q = 0; q < NTB; ++q) gthr |= (uint64_t)((tid >> q) & 1u) << P.qs[p0.tl[q]];
         }
+        mbar_wait(&mbar[j % NBUF], (uint32_t)((j / NBUF) & 1));
         if (init) {
             // the same addressing as a load, from a virtual memory holding init at init_index
             const uint64_t lt = ((base | gthr) ^ P.xm_load) & ~P.regm_load;
@@ -597,19 +696,16 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
             }
         } else {
             // the tile has landed in shared memory in logical order: read it in the phase-0 layout
-            cp_async_wait_all();
-            __syncthreads();
             uint32_t t0 = 0;
 #pragma unroll
-            for (int j = 0; j < NTB; ++j) t0 |= ((tid >> j) & 1u) << P.ph[0].tl[j];
+            for (int q = 0; q < NTB; ++q) t0 |= ((tid >> q) & 1u) << P.ph[0].tl[q];
+            t0 = swz(t0) * (uint32_t)sizeof(V);
 #pragma unroll
-            t0 = swz(t0);
-#pragma unroll
-            for (int r = 0; r < NR; ++r) a[r] = sm[t0 ^ P.ph[0].so[r]];
-            if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: prefetch right away
-                __syncthreads();
-                if (Tn < P.ntiles) prefetch_tile(sm, psi, Tn, P, gt, tid);
-            }
+            for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + (t0 ^ P.ph[0].so[r]));
+        }
+        if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: release the buffer right away
+            named_bar(bar);
+            issue_tile(smbase, mbar, psi, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
         }
 
         // ONE flat loop over records; a phase change is just a record (C_XPOSE) so that all paths
@@ -618,7 +714,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
         uint32_t ph = 0;
         uint64_t lbase = base;
 #pragma unroll
-        for (int j = 0; j < NTB; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[P.ph[0].tl[j]];
+        for (int q = 0; q < NTB; ++q) lbase |= (uint64_t)((tid >> q) & 1u) << P.qs[P.ph[0].tl[q]];
         // records are fetched as one 64-bit constant load, one record ahead (the fetch -> decode
         // -> branch chain was the top stall in ncu's source view; a shared-memory copy fetched by
         // a volatile load at the top of the iteration measured ~6 % slower)
@@ -642,23 +738,23 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 ph = g.a;
                 uint32_t tt = 0;
 #pragma unroll
-                for (int j = 0; j < NTB; ++j) tt |= ((tid >> j) & 1u) << prv.tl[j];
+                for (int q = 0; q < NTB; ++q) tt |= ((tid >> q) & 1u) << prv.tl[q];
                 // g.b = 1: same thread-bit layout on both sides -- every thread writes and reads
                 // back only its own slots (a register permutation), no barrier needed
-                if (!g.b) __syncthreads();
-                tt = swz(tt);
-#define TQ_ST(r) if constexpr (r < NR) sm[tt ^ prv.so_out[r]] = a[r];
+                if (!g.b) named_bar(bar);
+                tt = swz(tt) * (uint32_t)sizeof(V);
+#define TQ_ST(r) if constexpr (r < NR) *reinterpret_cast<V *>(smb + (tt ^ prv.so_out[r])) = a[r];
                 TQ_ST(0) TQ_ST(1) TQ_ST(2) TQ_ST(3) TQ_ST(4) TQ_ST(5) TQ_ST(6) TQ_ST(7)
                 TQ_ST(8) TQ_ST(9) TQ_ST(10) TQ_ST(11) TQ_ST(12) TQ_ST(13) TQ_ST(14) TQ_ST(15)
                 TQ_ST(16) TQ_ST(17) TQ_ST(18) TQ_ST(19) TQ_ST(20) TQ_ST(21) TQ_ST(22) TQ_ST(23)
                 TQ_ST(24) TQ_ST(25) TQ_ST(26) TQ_ST(27) TQ_ST(28) TQ_ST(29) TQ_ST(30) TQ_ST(31)
 #undef TQ_ST
-                if (!g.b) __syncthreads();
+                if (!g.b) named_bar(bar);
                 tt = 0;
 #pragma unroll
-                for (int j = 0; j < NTB; ++j) tt |= ((tid >> j) & 1u) << cur.tl[j];
-                tt = swz(tt);
-#define TQ_LD(r) if constexpr (r < NR) a[r] = sm[tt ^ cur.so[r]];
+                for (int q = 0; q < NTB; ++q) tt |= ((tid >> q) & 1u) << cur.tl[q];
+                tt = swz(tt) * (uint32_t)sizeof(V);
+#define TQ_LD(r) if constexpr (r < NR) a[r] = *reinterpret_cast<const V *>(smb + (tt ^ cur.so[r]));
                 TQ_LD(0) TQ_LD(1) TQ_LD(2) TQ_LD(3) TQ_LD(4) TQ_LD(5) TQ_LD(6) TQ_LD(7)
                 TQ_LD(8) TQ_LD(9) TQ_LD(10) TQ_LD(11) TQ_LD(12) TQ_LD(13) TQ_LD(14) TQ_LD(15)
                 TQ_LD(16) TQ_LD(17) TQ_LD(18) TQ_LD(19) TQ_LD(20) TQ_LD(21) TQ_LD(22) TQ_LD(23)
@@ -667,10 +763,10 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
                 // logical index bits of this thread (thread + outer bits) for predicates
                 lbase = base;
 #pragma unroll
-                for (int j = 0; j < NTB; ++j) lbase |= (uint64_t)((tid >> j) & 1u) << P.qs[cur.tl[j]];
-                if (gi == P.last_xpose && !init) {   // shared memory is free until the next tile
-                    __syncthreads();
-                    if (Tn < P.ntiles) prefetch_tile(sm, psi, Tn, P, gt, tid);
+                for (int q = 0; q < NTB; ++q) lbase |= (uint64_t)((tid >> q) & 1u) << P.qs[cur.tl[q]];
+                if (gi == P.last_xpose) {   // the buffer is free until tile j + NBUF: hand it over
+                    named_bar(bar);
+                    issue_tile(smbase, mbar, psi, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
                 }
             }
         }
@@ -679,7 +775,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
         const Phase &last = P.ph[P.nphase - 1];
         gthr = 0;
 #pragma unroll
-        for (int j = 0; j < NTB; ++j) gthr |= (uint64_t)((tid >> j) & 1u) << P.qs[last.tl[j]];
+        for (int q = 0; q < NTB; ++q) gthr |= (uint64_t)((tid >> q) & 1u) << P.qs[last.tl[q]];
         if (P.flags & F_SCALE) {
             const R sr = (R)P.scale_re, si = (R)P.scale_im;
             if (si == R(0)) {
@@ -704,7 +800,7 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
             }
         } else {
 #pragma unroll
-            for (int r = 0; r < NR; ++r) __stcs(q0 + P.gs[r], a[r]);
+            for (int r = 0; r < NR; ++r) __stcs(reinterpret_cast<V *>(reinterpret_cast<char *>(q0) + P.gs[r]), a[r]);
         }
         if (P.flags & F_SUMS) {
             double s = 0.0;
@@ -715,15 +811,15 @@ __global__ void __launch_bounds__(NT) k_fused(typename CV<R>::T *__restrict__ ps
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-            if ((tid & 31) == 0) red[tid >> 5] = s;
-            __syncthreads();
+            if ((tid & 31) == 0) red[grp][tid >> 5] = s;
+            named_bar(bar);
             if (tid == 0) {
                 double t = 0.0;
 #pragma unroll
-                for (int w = 0; w < NT / 32; ++w) t += red[w];
+                for (int w = 0; w < NT / 32; ++w) t += red[grp][w];
                 sums[(base ^ P.xm_store) >> TB] = t;
             }
-            __syncthreads();
+            named_bar(bar);
         }
     }
 }
@@ -1009,7 +1105,7 @@ static int rec_nparams(uint16_t c)
     if (c >= C_TD1 && c < C_TPH) return 2;
     if (c == C_TPH) return 4;
     if (c >= C_DK && c < C_CX2) return 2 << __builtin_popcount(c - C_DK);
-    if (c >= C_CU && c < C_N) return 32;
+    if (c >= C_CU && c < C_CCX) return 32;
     return 0;
 }
 
@@ -1018,12 +1114,18 @@ static bool is_perm_rec(uint16_t c)
     if (c >= C_X && c < C_X + 5) return true;
     if (c >= C_CX && c < C_CX + 25) return (c - C_CX) / 5 != (c - C_CX) % 5;
     if (c >= C_CX2 && c < C_CU) return code_ok(c);
+    if (c >= C_CCX && c < C_N) return code_ok(c);
     return false;
 }
 
 static uint32_t perm_apply(uint16_t c, uint32_t r)
 {
     if (c < C_X + 5) return r ^ (1u << (c - C_X));
+    if (c >= C_CCX) {
+        const int p = (c - C_CCX) / 6;
+        const uint32_t cm = (uint32_t)hdh_mask(p, (c - C_CCX) % 6) & ~(1u << p);
+        return (r & cm) == cm ? r ^ (1u << p) : r;
+    }
     if (c >= C_CX2) {
         const uint32_t cb = (c - C_CX2) / 25, t1 = (c - C_CX2) / 5 % 5, t2 = (c - C_CX2) % 5;
         return ((r >> cb) & 1) ? r ^ (1u << t1) ^ (1u << t2) : r;
@@ -1464,8 +1566,8 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                         // snap to the exact values the algebra gives (errors <= a few ulp)
                         for (double &v : e) {
                             if (fabs(v) < 1e-15) v = 0.0;
-                            else if (fabs(v - 1.0) < 4e-16) v = 1.0;
-                            else if (fabs(v + 1.0) < 4e-16) v = -1.0;
+                            else if (fabs(v - 1.0) < 1e-15) v = 1.0;    // <= 4 ulp
+                            else if (fabs(v + 1.0) < 1e-15) v = -1.0;
                         }
                         const bool offz = e[2] == 0 && e[3] == 0 && e[4] == 0 && e[5] == 0;
                         const bool diagz = e[0] == 0 && e[1] == 0 && e[6] == 0 && e[7] == 0;
@@ -1480,11 +1582,23 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                     }
                     GRec r;
                     memset(&r, 0, sizeof(r));
-                    r.code = (uint16_t)(C_CU + 6 * p + jj);
-                    r.a = (uint8_t)unit;
-                    r.b = (uint8_t)kinds;
-                    r.pi = (uint16_t)prm.size();
-                    prm.insert(prm.end(), blk.begin(), blk.end());
+                    static const bool no_ccx = getenv("TUSQ_NO_CCX") != nullptr;
+                    if (getenv("TUSQ_DEBUG_PLAN")) {
+                        fprintf(stderr, "  cu p %d j %d kinds %x unit %x t2 %d:", p, jj, kinds, unit, t2 != nullptr);
+                        for (int q = 0; q < 32; ++q) fprintf(stderr, " %.3g", blk[q] - (fabs(blk[q]) > 0.5 ? (blk[q] > 0 ? 1 : -1) : 0));
+                        fprintf(stderr, "\n");
+                    }
+                    if (!no_ccx && kinds == (2u << 6) && unit == 8u && code_ok(C_CCX + 6 * p + jj)) {
+                        // an error-free Toffoli: a pure register permutation (compile-time swaps,
+                        // no block dispatch; absorbable into phase entry/exit offsets)
+                        r.code = (uint16_t)(C_CCX + 6 * p + jj);
+                    } else {
+                        r.code = (uint16_t)(C_CU + 6 * p + jj);
+                        r.a = (uint8_t)unit;
+                        r.b = (uint8_t)kinds;
+                        r.pi = (uint16_t)prm.size();
+                        prm.insert(prm.end(), blk.begin(), blk.end());
+                    }
                     m.push_back(r);
                     for (int b = 0; b < RB; ++b)
                         if ((xo >> b) & 1u) {
@@ -1704,13 +1818,13 @@ static int blocks_per_sm(int prec)
     static int occ[2] = {0, 0};
     int &o = occ[prec == 128 ? 1 : 0];
     if (!o) {
-        size_t smem = (size_t)(1 << TB) * (prec == 128 ? 16 : 8);
+        size_t smem = (size_t)NBUF * (1 << TB) * (prec == 128 ? 16 : 8);
         if (prec == 128) {
             cudaFuncSetAttribute(k_fused<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused<double>, NT, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused<double>, NT * NG, smem);
         } else {
             cudaFuncSetAttribute(k_fused<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused<float>, NT, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused<float>, NT * NG, smem);
         }
         if (o < 1) o = 1;
     }
@@ -1853,13 +1967,38 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         const double bytes = pending_init ? s : 2 * s;
         if (!ctx.dry) {
             int bps = blocks_per_sm(prec_);
-            uint64_t grid = std::min<uint64_t>(P.ntiles, (uint64_t)device_sm_count() * bps);
-            size_t smem = (size_t)(1 << TB) * (prec_ == 128 ? 16 : 8);
+            uint64_t grid = std::min<uint64_t>((P.ntiles + NG - 1) / NG, (uint64_t)device_sm_count() * bps);
+            size_t smem = (size_t)NBUF * (1 << TB) * (prec_ == 128 ? 16 : 8);
+            // incremental tile bases (deposited steps) and byte offsets for the kernel
+            P.outer = ((n_ == 64 ? ~0ull : (1ull << n_) - 1)) & ~B.tile;
+            auto pdep = [&](uint64_t x) {
+                uint64_t o = 0;
+                for (uint32_t q = 0; q < n_ && x; ++q)
+                    if (P.outer & bit(q)) { o |= (x & 1) << q; x >>= 1; }
+                return o;
+            };
+            const uint64_t S = grid * NG;
+            P.dstep = pdep(S);
+            for (int g = 0; g < NG; ++g) {
+                const uint64_t gn = (uint64_t)g + NBUF;
+                P.dissue[g] = pdep((gn % NG) + (gn / NG) * S - (uint64_t)g);
+            }
+            const uint32_t esz = prec_ == 128 ? 16 : 8;
+            for (int r = 0; r < NR; ++r) {
+                P.gs[r] *= esz;
+                P.gj[r] *= esz;
+                P.sj[r] = (uint16_t)(P.sj[r] * esz);
+            }
+            for (uint32_t k = 0; k < P.nphase; ++k)
+                for (int r = 0; r < NR; ++r) {
+                    P.ph[k].so[r] = (uint16_t)(P.ph[k].so[r] * esz);
+                    P.ph[k].so_out[r] = (uint16_t)(P.ph[k].so_out[r] * esz);
+                }
             if (ctx.timer) ctx.timer->begin(ctx.st);
             if (prec_ == 128)
-                k_fused<double><<<(unsigned)grid, NT, smem, ctx.st>>>((double2 *)ctx.psi, P, d_sums);
+                k_fused<double><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((double2 *)ctx.psi, P, d_sums);
             else
-                k_fused<float><<<(unsigned)grid, NT, smem, ctx.st>>>((float2 *)ctx.psi, P, d_sums);
+                k_fused<float><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((float2 *)ctx.psi, P, d_sums);
             static const bool sync_launch = getenv("TUSQ_SYNC_LAUNCH") != nullptr;   // measurement aid
             if (sync_launch) cudaStreamSynchronize(ctx.st);
             if (ctx.timer) {
@@ -1871,7 +2010,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                         const uint16_t c = P.g[i].code;
                         int k = c < C_U ? 0 : (c >= C_DK && c < C_CX2) ? 1 : ((c >= C_CX && c < C_CPH) || (c >= C_CX2 && c < C_CU)) ? 2
                                 : (c >= C_D1 && c < C_CX) ? 3 : c == C_XPOSE ? 4 : (c >= C_X && c < C_D1) ? 5
-                                : (c >= C_TX && c <= C_TPH) ? 6 : (c >= C_CU && c < C_N) ? 8 : 7;
+                                : (c >= C_TX && c <= C_TPH) ? 6 : (c >= C_CU && c < C_CCX) ? 8 : (c >= C_CCX && c < C_N) ? 2 : 7;
                         cnt[k]++;
                     }
                     snprintf(tag, sizeof(tag), "ops %zu recs %u ph %u init %d tile %#llx H%d DK%d CX%d D%d XP%d XY%d T%d O%d CU%d",
