@@ -47,7 +47,7 @@ typedef enum {
     TUSQ_ERR_UNSUPPORTED = 2,   /* valid request this build does not implement */
     TUSQ_ERR_OOM = 3,           /* host or device allocation failed */
     TUSQ_ERR_CUDA = 4,          /* CUDA runtime error (incl. no device) */
-    TUSQ_ERR_NCCL = 5,          /* reserved for the multi-GPU collectives */
+    TUSQ_ERR_NCCL = 5,          /* NCCL missing or a collective failed (sharded mode) */
     TUSQ_ERR_CAPACITY = 6,      /* state buffer smaller than 2^n * bytes per amplitude */
     TUSQ_ERR_INTERNAL = 7
 } tusq_status;
@@ -79,6 +79,8 @@ typedef struct { double p1, p2, p_meas; uint32_t flags, _pad; } tusq_noise;
 typedef struct { uint32_t alpha_num, alpha_den, beta, enabled; } tusq_prune;
 
 typedef struct tusq_tree tusq_tree;
+/* Communicator of the sharded mode: library-owned, freed with tusq_comm_free. */
+typedef struct tusq_comm tusq_comm;
 
 typedef struct {
     uint64_t S1, S2, S3;          /* shots, unique raw ERs (tallying), unique canonical ERs (commutation) */
@@ -100,13 +102,21 @@ typedef struct {
 #define TUSQ_EXEC_CONTINUE    0x40u /* d_state already holds the final state of leaf leaf_begin-1 (left by a
                                        previous call): continue the DFS from there instead of re-anchoring */
 
+/* exec.mode */
+#define TUSQ_MODE_REPLICA 0u    /* the whole 2^n vector on this device (leaf ranges shard across replicas) */
+#define TUSQ_MODE_SHARDED 1u    /* amplitudes split over comm->nranks shards by the high (global) qubits;
+                                   every rank runs the same leaves; slots are summed over ranks */
+
 typedef struct {
     uint32_t precision;         /* 128 (complex128) or 64 (complex64) */
-    uint32_t mode;              /* 0 = replica (whole vector on this device) */
+    uint32_t mode;              /* TUSQ_MODE_REPLICA or TUSQ_MODE_SHARDED */
     int32_t  device;            /* CUDA device ordinal; -1 = current */
     uint32_t flags;             /* TUSQ_EXEC_* */
     void    *d_state;           /* caller-owned device buffer of >= 2^n * (precision/8) bytes, or NULL
-                                   (library allocates and frees it inside the call) */
+                                   (library allocates and frees it inside the call).  Sharded mode: this
+                                   process's shards, 2^(n-g) amplitudes each (g = log2 nranks): one shard
+                                   (NCCL communicator) or all nranks back to back (local communicator);
+                                   on return they hold the canonical layout (shard r = global bits r) */
     uint64_t state_bytes;       /* size of d_state */
     void    *stream;            /* cudaStream_t; NULL = legacy default stream */
     uint64_t leaf_begin;        /* DFS leaf range [leaf_begin, leaf_end) to run; */
@@ -116,6 +126,7 @@ typedef struct {
     uint32_t fuse_qubits;       /* tile qubits of the fused kernel; 0 = default (12) */
     uint32_t _pad;
     double   edge_eps;          /* edge-draw window (0 = 1e-9 for c128, 1e-5 for c64) */
+    tusq_comm *comm;            /* TUSQ_MODE_SHARDED: the communicator (NULL otherwise) */
 } tusq_exec;
 
 typedef struct {
@@ -133,6 +144,7 @@ typedef struct {
     double   gate_kernel_seconds;   /* TUSQ_EXEC_PROFILE: summed CUDA-event durations of those launches */
     double   gate_kernel_bytes;     /* algorithmic HBM bytes of those launches */
     uint64_t fused_launches;        /* K5 launches among `launches` */
+    uint64_t exchanges;             /* sharded mode: global<->local qubit swaps (NCCL send/recv of half shards) */
 } tusq_run_stats;
 
 /* ECM + tree.  ops: n_ops gates (host).  seed keys every Philox stream.
@@ -167,6 +179,18 @@ void tusq_tree_free(tusq_tree *tree);
  * On return d_state holds the final state of the last leaf run.  stats may be NULL. */
 tusq_status tusq_run_tree(const tusq_tree *tree, const tusq_exec *exec, uint64_t *out_slots,
                           tusq_run_stats *stats);
+
+/* Sharded mode communicators (34q QFT at c128 = 256 GiB over 8 B200s).
+ *   tusq_comm_unique_id  ncclGetUniqueId on one rank; broadcast the 128 bytes to the others.
+ *   tusq_comm_init       one process per GPU: ncclCommInitRank(nranks, id, rank) on `device`.
+ *   tusq_comm_init_local all nshards shards in THIS process on one device (exchanges are device
+ *                        swaps): the same sharded logic, testable on one GPU.
+ * nranks / nshards must be a power of two >= 2.  NCCL is loaded at run time (libnccl.so.2);
+ * TUSQ_ERR_NCCL if it is missing or a collective fails. */
+tusq_status tusq_comm_unique_id(uint8_t out[128]);
+tusq_status tusq_comm_init(const uint8_t id[128], int nranks, int rank, int device, tusq_comm **out);
+tusq_status tusq_comm_init_local(int nshards, int device, tusq_comm **out);
+void tusq_comm_free(tusq_comm *comm);
 
 /* Inverse-CDF draws from |amp|^2 of a device state: draw j uses Philox counter
  * (j, leaf_lo, leaf_hi, 0x53000000) keyed by seed, u = (x >> 11) 2^-53, t = u * sum|amp|^2,

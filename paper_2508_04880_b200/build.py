@@ -54,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and out:
             sys.stderr.write(out)
     tmp = LIB + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread"])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread", "-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -236,7 +236,14 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     auto t0 = std::chrono::steady_clock::now();
     if (!t || !ex) return fail(TUSQ_ERR_INVALID_ARG, "NULL argument");
     if (!prec_ok(ex->precision)) return fail(TUSQ_ERR_INVALID_ARG, "precision must be 128 or 64");
-    if (ex->mode != 0) return fail(TUSQ_ERR_UNSUPPORTED, "only replica mode (0) is implemented");
+    if (ex->mode == TUSQ_MODE_SHARDED) {
+        try {
+            return run_tree_sharded(t, ex, out_slots, stats_out);
+        } catch (const std::bad_alloc &) {
+            return fail(TUSQ_ERR_OOM, "host allocation failed in tusq_run_tree");
+        }
+    }
+    if (ex->mode != TUSQ_MODE_REPLICA) return fail(TUSQ_ERR_INVALID_ARG, "mode must be TUSQ_MODE_REPLICA or TUSQ_MODE_SHARDED");
     const bool dry = ex->flags & TUSQ_EXEC_PLAN_ONLY;
     const bool sample = !(ex->flags & TUSQ_EXEC_NO_SAMPLE);
     if (sample && !dry && !out_slots) return fail(TUSQ_ERR_INVALID_ARG, "out_slots is NULL");

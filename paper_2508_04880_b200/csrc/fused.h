@@ -70,4 +70,7 @@ private:
 // one kernel per gate (K1-K4); consecutive Paulis on distinct qubits merge into one K4 pass
 void execute_unfused(const std::vector<Op> &ops, Ctx &ctx);
 
+// tusq_run_tree in TUSQ_MODE_SHARDED (sharded.cu)
+tusq_status run_tree_sharded(const tusq_tree *t, const tusq_exec *ex, uint64_t *out_slots, tusq_run_stats *stats);
+
 }  // namespace tq

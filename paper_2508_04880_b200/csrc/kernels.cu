@@ -421,8 +421,12 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
                                                const double *__restrict__ phys, const double *__restrict__ sprefix,
                                                uint64_t nb, uint64_t n_draws, uint32_t k0, uint32_t k1,
                                                uint64_t leaf, double edge_eps, uint64_t xm,
-                                               uint64_t *__restrict__ out, uint32_t *__restrict__ edges)
+                                               uint64_t *__restrict__ out, uint32_t *__restrict__ edges,
+                                               double tg_total, double tg_lo, double tg_hi, uint64_t ohi)
 {
+    // sharded mode (tg_total > 0): the draw's point t = u * tg_total on the CDF over all shards in
+    // logical order; this shard owns [tg_lo, tg_hi) and searches t - tg_lo locally, writing
+    // ohi | local index (ohi = the shard's global bits)
     // logical index i is stored at physical i ^ xm (pending X relabels of the fused path)
     using V = typename CV<R>::T;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -433,7 +437,14 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
     const uint64_t nsb = (nb + SB - 1) / SB;
     const uint64_t mh = xm >> block_bits;
     const double T = sprefix[nsb];
-    const double t = (double)(x >> 11) * 0x1.0p-53 * T;
+    double t;
+    if (tg_total > 0.0) {
+        const double tg = (double)(x >> 11) * 0x1.0p-53 * tg_total;
+        if (!(tg >= tg_lo && tg < tg_hi)) return;   // another shard's draw (warp-uniform)
+        t = tg - tg_lo;
+    } else {
+        t = (double)(x >> 11) * 0x1.0p-53 * T;
+    }
     // superblock: first sb whose inclusive prefix sprefix[sb+1] exceeds t
     uint64_t lo = 0, hi = nsb - 1;
     while (lo < hi) {
@@ -511,7 +522,7 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
             k = b * bs + kk;
             double gap = fmin(t - prev, run - t);
             edge = !found || gap < edge_eps;
-            out[warp] = k;
+            out[warp] = k | ohi;
             if (edge) atomicAdd(edges, 1u);
         }
     } else {
@@ -522,7 +533,7 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
                 V a = blk[i];
                 if (a.x != 0 || a.y != 0) { kk = i; break; }
             }
-            out[warp] = b * bs + kk;
+            out[warp] = (b * bs + kk) | ohi;
             atomicAdd(edges, 1u);
         }
     }
@@ -538,10 +549,29 @@ double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, 
     uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
     if (prec == 64)
         k_draws<float><<<grid, TPB, 0, st>>>((const float2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0, k1,
-                                             leaf, edge_eps, xm, d_out, d_edges);
+                                             leaf, edge_eps, xm, d_out, d_edges, 0.0, 0.0, 0.0, 0);
     else
         k_draws<double><<<grid, TPB, 0, st>>>((const double2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0,
-                                              k1, leaf, edge_eps, xm, d_out, d_edges);
+                                              k1, leaf, edge_eps, xm, d_out, d_edges, 0.0, 0.0, 0.0, 0);
+    return (double)n_draws * (double)(1ull << block_bits) * (prec == 64 ? 8.0 : 16.0);
+}
+
+// sharded mode: the draws of one leaf that fall into this shard's CDF window [t_lo, t_hi)
+double launch_draws_window(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
+                           const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, double edge_eps,
+                           uint64_t *d_out, uint32_t *d_edges, double t_total, double t_lo, double t_hi, uint64_t ohi,
+                           cudaStream_t st)
+{
+    if (!n_draws) return 0.0;
+    uint64_t nb = 1ull << (n - block_bits);
+    unsigned grid = (unsigned)((n_draws * 32 + TPB - 1) / TPB);
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    if (prec == 64)
+        k_draws<float><<<grid, TPB, 0, st>>>((const float2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0, k1,
+                                             leaf, edge_eps, 0, d_out, d_edges, t_total, t_lo, t_hi, ohi);
+    else
+        k_draws<double><<<grid, TPB, 0, st>>>((const double2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0,
+                                              k1, leaf, edge_eps, 0, d_out, d_edges, t_total, t_lo, t_hi, ohi);
     return (double)n_draws * (double)(1ull << block_bits) * (prec == 64 ? 8.0 : 16.0);
 }
 

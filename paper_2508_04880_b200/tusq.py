@@ -43,7 +43,7 @@ class Exec(C.Structure):
     _fields_ = [("precision", C.c_uint32), ("mode", C.c_uint32), ("device", C.c_int32), ("flags", C.c_uint32),
                 ("d_state", C.c_void_p), ("state_bytes", C.c_uint64), ("stream", C.c_void_p),
                 ("leaf_begin", C.c_uint64), ("leaf_end", C.c_uint64), ("reanchor_budget", C.c_uint64),
-                ("fuse_qubits", C.c_uint32), ("_pad", C.c_uint32), ("edge_eps", C.c_double)]
+                ("fuse_qubits", C.c_uint32), ("_pad", C.c_uint32), ("edge_eps", C.c_double), ("comm", C.c_void_p)]
 
 
 class RunStats(C.Structure):
@@ -52,7 +52,7 @@ class RunStats(C.Structure):
                 ("edge_draws", C.c_uint64), ("hbm_bytes", C.c_double), ("sample_bytes", C.c_double),
                 ("host_seconds", C.c_double), ("gate_kernel_launches", C.c_uint64),
                 ("gate_kernel_seconds", C.c_double), ("gate_kernel_bytes", C.c_double),
-                ("fused_launches", C.c_uint64)]
+                ("fused_launches", C.c_uint64), ("exchanges", C.c_uint64)]
 
     def to_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -70,16 +70,22 @@ _sigs = {
     "tusq_sample": [_vp, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, _vp, _vp],
     "tusq_apply_ops": [_vp, C.c_uint32, C.c_uint32, _vp, C.c_uint64, C.c_uint32, _vp],
     "tusq_init_basis": [_vp, C.c_uint32, C.c_uint32, C.c_uint64, C.c_double, C.c_double, _vp],
+    "tusq_comm_unique_id": [_vp],
+    "tusq_comm_init": [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
+    "tusq_comm_init_local": [C.c_int, C.c_int, C.POINTER(_vp)],
 }
 for _name, _args in _sigs.items():
     getattr(_lib, _name).argtypes = _args
     getattr(_lib, _name).restype = C.c_int
 _lib.tusq_tree_free.argtypes = [_vp]
 _lib.tusq_tree_free.restype = None
+_lib.tusq_comm_free.argtypes = [_vp]
+_lib.tusq_comm_free.restype = None
 _lib.tusq_last_error.restype = C.c_char_p
 _lib.tusq_version.restype = C.c_char_p
 
-EXPORTED = list(_sigs) + ["tusq_tree_free", "tusq_last_error", "tusq_version"]
+EXPORTED = list(_sigs) + ["tusq_tree_free", "tusq_comm_free", "tusq_last_error", "tusq_version"]
+MODE_REPLICA, MODE_SHARDED = 0, 1
 
 
 class TusqError(RuntimeError):
@@ -175,18 +181,59 @@ def build_error_tree(n: int, ops, p1: float, p2: float, p_meas: float, shots: in
 
 def run_tree(tree: Tree, precision: int = 128, d_state=None, state_bytes: int = 0, stream=None,
              leaf_begin: int = 0, leaf_end: int = 0, flags: int = 0, reanchor_budget: int = 0,
-             fuse_qubits: int = 0, edge_eps: float = 0.0, device: int = -1, out_slots: Optional[np.ndarray] = None):
-    """Returns (slots u64[S1], stats dict).  d_state: device pointer (int) or tensor; None = library-allocated."""
+             fuse_qubits: int = 0, edge_eps: float = 0.0, device: int = -1, out_slots: Optional[np.ndarray] = None,
+             comm: Optional["Comm"] = None):
+    """Returns (slots u64[S1], stats dict).  d_state: device pointer (int) or tensor; None = library-allocated.
+    comm: a Comm -> TUSQ_MODE_SHARDED (d_state then holds this process's shards)."""
     info = tree.info()
     if out_slots is None:
         out_slots = np.zeros(info["S1"], dtype=np.uint64)
     if d_state is not None and not state_bytes and hasattr(d_state, "numel"):
         state_bytes = d_state.numel() * d_state.element_size()
-    ex = Exec(precision, 0, device, flags, _ptr(d_state), state_bytes, _ptr(stream), leaf_begin, leaf_end,
-              reanchor_budget, fuse_qubits, 0, edge_eps)
+    ex = Exec(precision, MODE_SHARDED if comm is not None else MODE_REPLICA, device, flags, _ptr(d_state),
+              state_bytes, _ptr(stream), leaf_begin, leaf_end, reanchor_budget, fuse_qubits, 0, edge_eps,
+              comm.h if comm is not None else None)
     stats = RunStats()
     _check(_lib.tusq_run_tree(tree.h, C.byref(ex), out_slots.ctypes.data_as(_u64p), C.byref(stats)), "tusq_run_tree")
     return out_slots, stats.to_dict()
+
+
+class Comm:
+    """Sharded-mode communicator (tusq_comm): Comm.local(nshards) drives all shards from this process
+    on one device; Comm.nccl(uid, nranks, rank, device) is one rank of a one-process-per-GPU job."""
+
+    def __init__(self, h: int, nranks: int):
+        self.h, self.nranks = h, nranks
+
+    @staticmethod
+    def unique_id() -> bytes:
+        b = (C.c_uint8 * 128)()
+        _check(_lib.tusq_comm_unique_id(C.cast(b, _vp)), "tusq_comm_unique_id")
+        return bytes(b)
+
+    @classmethod
+    def nccl(cls, uid: bytes, nranks: int, rank: int, device: int = -1) -> "Comm":
+        b = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = _vp()
+        _check(_lib.tusq_comm_init(C.cast(b, _vp), nranks, rank, device, C.byref(h)), "tusq_comm_init")
+        return cls(h.value, nranks)
+
+    @classmethod
+    def local(cls, nshards: int, device: int = -1) -> "Comm":
+        h = _vp()
+        _check(_lib.tusq_comm_init_local(nshards, device, C.byref(h)), "tusq_comm_init_local")
+        return cls(h.value, nshards)
+
+    def free(self):
+        if self.h:
+            _lib.tusq_comm_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def sample(d_state, n: int, precision: int, n_draws: int, seed: int, leaf: int, d_out, stream=None):

@@ -140,3 +140,26 @@ def test_partition_contiguous_and_balanced(lib):
     for nr in (1, 2, 4, 8):
         b = t.partition(nr)
         assert b[0] == 0 and b[-1] == nl and np.all(np.diff(b.astype(np.int64)) >= 0)
+
+
+def test_sharded_plan_only(lib):
+    # sharded mode's host logic (no device): same scheduler as replica mode (gate applications,
+    # leaves), global<->local exchanges only where a dense gate meets a global qubit
+    for name in ("C2a", "C2b", "C3"):
+        cfg = W.config(name)
+        nz = cfg.noise
+        t = lib.build_error_tree(cfg.n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
+        _, rep = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY)
+        for R in (2, 4, 8):
+            _, s = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY, comm=lib.Comm.local(R))
+            assert s["gate_apps"] == rep["gate_apps"] and s["leaves"] == rep["leaves"]
+            assert s["draws"] == cfg.shots
+            assert s["exchanges"] > 0
+    # a circuit of diagonal / CX-from-global / X gates never exchanges
+    n = 8
+    ops = [W.op(W.H, 0), W.op(W.CX, 7, 0), W.op(W.X, 7), W.op(W.T, 6), W.op(W.CZ, 6, 1), W.op(W.CP, 7, 6, 0.3)]
+    t = lib.build_error_tree(n, ops, 0.0, 0.0, 0.0, 8, 1)
+    _, s = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY, comm=lib.Comm.local(4))
+    assert s["exchanges"] == 0
+    with pytest.raises(lib.TusqError):
+        lib.Comm.local(3)
