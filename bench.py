@@ -114,7 +114,8 @@ def cpu_oracle_rate(cfg, max_seconds: float = 20.0):
 
 def workload_desc(cfg) -> str:
     nz = cfg.noise
-    return (f"{cfg.name}: {cfg.n}q Cuccaro adder (L={len(cfg.ops)}), depolarizing p1={nz.p1} p2={nz.p2}"
+    kind = "Cuccaro adder" if cfg.name in ("C1", "C3", "C4") else ("GHZ" if cfg.name == "C2a" else "QFT")
+    return (f"{cfg.name}: {cfg.n}q {kind} (L={len(cfg.ops)}), depolarizing p1={nz.p1} p2={nz.p2}"
             + (f" p_meas={nz.p_meas}" if nz.p_meas else "") + f", {cfg.shots} shots, seed {cfg.seed}, alpha 1/100, beta 100")
 
 
@@ -172,6 +173,8 @@ def main():
     ap.add_argument("--no-fuse", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="replica", choices=["replica", "sharded"],
+                    help="sharded: amplitudes split over the N ranks by global qubits (e.g. --config C5 on 8 GPUs)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -198,17 +201,27 @@ def main():
     tree = T.build_error_tree(n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
     t_ecm = time.perf_counter() - t0
     info = tree.info()
-    bounds = tree.partition(world, prec)
-    lb, le = int(bounds[rank]), int(bounds[rank + 1])
     flags = T.EXEC_PROFILE | (T.EXEC_NO_FUSE if args.no_fuse else 0)
-    _, plan = T.run_tree(tree, prec, leaf_begin=lb, leaf_end=le, flags=flags | T.EXEC_PLAN_ONLY)
-    plan_bytes = plan["hbm_bytes"] + plan["sample_bytes"]
-
     dt = torch.complex128 if prec == 128 else torch.complex64
-    state = torch.empty(1 << n, dtype=dt, device="cuda")
+    comm = None
+    if args.mode == "sharded":
+        # every rank runs every leaf on its 2^(n-g) shard; the host plan is the same on all ranks
+        if world < 2:
+            raise SystemExit("--mode sharded needs >= 2 ranks (torch.distributed.run)")
+        from paper_2508_04880_b200 import dist as D
+        comm, _ = D.make_sharded_comm(local)
+        lb, le = 0, info["n_leaves"]
+        _, plan = T.run_tree(tree, prec, flags=flags | T.EXEC_PLAN_ONLY, comm=T.Comm.local(world))
+        state = torch.empty(1 << (n - (world.bit_length() - 1)), dtype=dt, device="cuda")
+    else:
+        bounds = tree.partition(world, prec)
+        lb, le = int(bounds[rank]), int(bounds[rank + 1])
+        _, plan = T.run_tree(tree, prec, leaf_begin=lb, leaf_end=le, flags=flags | T.EXEC_PLAN_ONLY)
+        state = torch.empty(1 << n, dtype=dt, device="cuda")
+    plan_bytes = plan["hbm_bytes"] + plan["sample_bytes"]
     stream = torch.cuda.current_stream()
     nleaf = max(le - lb, 1)
-    B = args.leaves_per_step or max(1, min(nleaf, 64 if n >= 28 else 256))
+    B = args.leaves_per_step or max(1, min(nleaf, (16 if comm is not None else 64) if n >= 28 else 256))
     slots = np.zeros(cfg.shots, dtype=np.uint64)
 
     # batches spread evenly over the rank's DFS range (the cost of a transition depends on where
@@ -221,7 +234,7 @@ def main():
         b = lb if full else lb + (s * stride) % nleaf
         e = le if full else min(b + B, le)
         _, st = T.run_tree(tree, prec, d_state=state, stream=stream, leaf_begin=b, leaf_end=e, flags=flags,
-                           out_slots=slots)
+                           out_slots=slots, comm=comm)
         return st
 
     order = list(range(nb_total))
@@ -272,7 +285,10 @@ def main():
                    "plan_gate_apps": plan["gate_apps"], "plan_hbm_GB": plan_bytes / 1e9,
                    "dftt_ops": info["dftt_ops"], "naive_ops": info["naive_ops"],
                    "l2": f"state {state.numel() * state.element_size() / 2**30:.0f} GiB >> 126 MB L2 (no flush needed)",
-                   "fused": not args.no_fuse, "parallelism": f"replica x{world}, contiguous DFS leaf ranges"},
+                   "fused": not args.no_fuse,
+                   "parallelism": (f"sharded x{world}: amplitudes split by {world.bit_length() - 1} global qubits, "
+                                   "NCCL half-shard exchanges" if comm is not None
+                                   else f"replica x{world}, contiguous DFS leaf ranges")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": ncu_traffic(prec, args.no_fuse),
                      "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one k_fused launch of this "
@@ -287,7 +303,7 @@ def main():
         "gpu_launches": int(tot["launches"]),
         "clocks": clk.summary(),
         "stats": {k: tot[k] for k in ("leaves", "resets", "gate_apps", "sweeps", "draws", "edge_draws",
-                                      "fused_launches")},
+                                      "fused_launches", "exchanges")},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         per, cores, desc = cpu_oracle_rate(cfg, args.cpu_seconds)

@@ -56,3 +56,27 @@ def run_tree_distributed(tree, precision: int = 128, d_state=None, stream=None, 
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
         slots = t.cpu().numpy().view(np.uint64)
     return slots, (lb, le)
+
+
+def share_unique_id(group=None, unique_id: Optional[Callable[[], bytes]] = None) -> bytes:
+    """Rank 0 draws the NCCL unique id (tusq_comm_unique_id); every rank receives it over the group."""
+    import torch.distributed as dist
+
+    from . import tusq as T
+
+    box = [(unique_id or T.Comm.unique_id)()] if dist.get_rank(group) == 0 else [None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    if not isinstance(box[0], (bytes, bytearray)) or len(box[0]) != 128:
+        raise RuntimeError("bad NCCL unique id")
+    return bytes(box[0])
+
+
+def make_sharded_comm(device: int, group=None, unique_id: Optional[Callable[[], bytes]] = None):
+    """Sharded mode: one tusq_comm per rank of the torch.distributed group, joined to the
+    library's own NCCL communicator (tusq_comm_init).  Returns (comm, uid bytes)."""
+    import torch.distributed as dist
+
+    from . import tusq as T
+
+    uid = share_unique_id(group, unique_id)
+    return T.Comm.nccl(uid, dist.get_world_size(group), dist.get_rank(group), device), uid

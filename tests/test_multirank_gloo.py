@@ -60,3 +60,41 @@ def test_gloo_world2_matches_single_rank(tmp_path, oracle, name):
     assert np.array_equal(s0, s1)
     ref, _ = oracle.Tree.from_config(W.config(name)).run()
     assert np.array_equal(s0, ref)
+
+
+def _sharded_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+
+    import paper_2508_04880_b200 as T
+    from paper_2508_04880_b200 import dist as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # the NCCL unique id travels over the process group (a stand-in id: no GPU/NCCL here)
+    uid = D.share_unique_id(unique_id=lambda: bytes(range(128)))
+    # every rank's sharded host plan is identical (deterministic, no communication)
+    cfg = W.config("C2b")
+    nz = cfg.noise
+    tree = T.build_error_tree(cfg.n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
+    _, st = T.run_tree(tree, 128, flags=T.EXEC_PLAN_ONLY, comm=T.Comm.local(world))
+    np.save(os.path.join(out_dir, f"uid{rank}.npy"), np.frombuffer(uid, dtype=np.uint8))
+    np.save(os.path.join(out_dir, f"plan{rank}.npy"), np.array([st["exchanges"], st["gate_apps"], st["hbm_bytes"]]))
+    # without a GPU the NCCL communicator must fail loudly (no silent fallback)
+    try:
+        T.Comm.nccl(uid, world, rank, 0)
+        ok = 1
+    except T.TusqError:
+        ok = 0
+    np.save(os.path.join(out_dir, f"nccl{rank}.npy"), np.array([ok]))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_plumbing(tmp_path, oracle):
+    port = _free_port()
+    mp.spawn(_sharded_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    u0, u1 = np.load(tmp_path / "uid0.npy"), np.load(tmp_path / "uid1.npy")
+    assert np.array_equal(u0, u1) and np.array_equal(u0, np.arange(128, dtype=np.uint8))
+    p0, p1 = np.load(tmp_path / "plan0.npy"), np.load(tmp_path / "plan1.npy")
+    assert np.array_equal(p0, p1) and p0[0] > 0
+    assert np.load(tmp_path / "nccl0.npy")[0] == 0 and np.load(tmp_path / "nccl1.npy")[0] == 0
