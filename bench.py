@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="replica", choices=["replica", "sharded"],
                     help="sharded: amplitudes split over the N ranks by global qubits (e.g. --config C5 on 8 GPUs)")
+    ap.add_argument("--shards", type=int, default=0,
+                    help="sharded mode on ONE GPU: this many shards driven by one process (local communicator)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -204,15 +206,21 @@ def main():
     flags = T.EXEC_PROFILE | (T.EXEC_NO_FUSE if args.no_fuse else 0)
     dt = torch.complex128 if prec == 128 else torch.complex64
     comm = None
+    nshards = 0
     if args.mode == "sharded":
         # every rank runs every leaf on its 2^(n-g) shard; the host plan is the same on all ranks
-        if world < 2:
-            raise SystemExit("--mode sharded needs >= 2 ranks (torch.distributed.run)")
-        from paper_2508_04880_b200 import dist as D
-        comm, _ = D.make_sharded_comm(local)
+        if world > 1:
+            from paper_2508_04880_b200 import dist as D
+            comm, _ = D.make_sharded_comm(local)
+            nshards = world
+            state = torch.empty(1 << (n - (world.bit_length() - 1)), dtype=dt, device="cuda")
+        else:
+            # one GPU: all shards in this process (the local communicator; exchanges are device swaps)
+            nshards = args.shards or 2
+            comm = T.Comm.local(nshards)
+            state = torch.empty(1 << n, dtype=dt, device="cuda")
         lb, le = 0, info["n_leaves"]
-        _, plan = T.run_tree(tree, prec, flags=flags | T.EXEC_PLAN_ONLY, comm=T.Comm.local(world))
-        state = torch.empty(1 << (n - (world.bit_length() - 1)), dtype=dt, device="cuda")
+        _, plan = T.run_tree(tree, prec, flags=flags | T.EXEC_PLAN_ONLY, comm=T.Comm.local(nshards))
     else:
         bounds = tree.partition(world, prec)
         lb, le = int(bounds[rank]), int(bounds[rank + 1])
@@ -286,8 +294,10 @@ def main():
                    "dftt_ops": info["dftt_ops"], "naive_ops": info["naive_ops"],
                    "l2": f"state {state.numel() * state.element_size() / 2**30:.0f} GiB >> 126 MB L2 (no flush needed)",
                    "fused": not args.no_fuse,
-                   "parallelism": (f"sharded x{world}: amplitudes split by {world.bit_length() - 1} global qubits, "
-                                   "NCCL half-shard exchanges" if comm is not None
+                   "parallelism": (f"sharded x{nshards} over {world} GPU(s): amplitudes split by "
+                                   f"{nshards.bit_length() - 1} global qubits, half-shard exchanges "
+                                   + ("(NCCL)" if world > 1 else "(local communicator, device swaps)")
+                                   if comm is not None
                                    else f"replica x{world}, contiguous DFS leaf ranges")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": ncu_traffic(prec, args.no_fuse),

@@ -79,6 +79,10 @@ def main():
                                          (W.op(W.CX, q, q + 1), W.op(W.T, q + 1), W.op(W.CX, q, q + 1),
                                           W.op(W.TDG, q))] * 4,
         "K5 4 Toffoli (CU records)": [g for g in W.adder(14)[1] if g[0] != W.X][4 * 17 + 2: 4 * 17 + 17],
+        # tile span vs transposes: 9 H over 9 consecutive qubits, 2 phases (pages per tile 1 / 8 / 512)
+        "K5 9 H on 8-16, 2 phases": [W.op(W.H, q) for q in range(8, 17)],
+        "K5 9 H on 14-22, 2 phases": [W.op(W.H, q) for q in range(14, 23)],
+        "K5 9 H on 20-28, 2 phases": [W.op(W.H, q) for q in range(20, 29)],
     }
     gx = [g for g in W.adder(14)[1] if g[0] != W.X]
     for k in (8, 9, 10):
