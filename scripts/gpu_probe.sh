@@ -1,0 +1,14 @@
+#!/bin/bash
+# Probe session: K5 anatomy under ncu (2 vs 3 phases), launch-trace fit, sharded bench on one GPU.
+cd $GRAFT_REPO_ROOT
+TAG=${1:-probe}
+O=gpurun_out/$TAG
+mkdir -p $O
+timeout 300 python scripts/kernel_bench.py > $O/kernels.json 2> $O/kernels.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 21 -c 8 -o $O/prof_phases \
+  python scripts/kernel_bench.py > $O/ncu_phases.log 2>&1
+timeout 600 python scripts/trace_groups.py > $O/trace.log 2>&1
+python scripts/fit_trace.py $O/trace.log > $O/fit.txt 2>&1
+timeout 900 python bench.py --config C3 --mode sharded --shards 8 --no-cpu-baseline > $O/bench_c3_sharded8.log 2>&1
+timeout 900 python bench.py --config C3 --no-cpu-baseline > $O/bench_c3_replica.log 2>&1
+echo done
