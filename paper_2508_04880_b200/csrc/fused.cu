@@ -124,6 +124,8 @@ struct Params {
     uint32_t rx;                  // register bits where xm_load is set (folded into gl, kept 0)
     uint16_t mloc;                // tile-local bits of xm_load (applied when copying to shared memory)
     uint16_t last_xpose;          // record index of the last transpose (0xFFFF: none)
+    uint16_t gtab;                // 0xFFFF, or: prm + gtab holds a u16[NR][NT] gather table (byte offsets):
+                                  // the phase-0 read takes register r of thread t from slot gtab[r][t]
     uint16_t st_pair;             // 0, or v: registers r, r ^ v hold adjacent amplitudes in the last
                                   // layout -> one 2x-wide store per pair
     uint32_t st_odd;              // bit r: register r holds the odd one of its pair
@@ -655,6 +657,13 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
     const uint32_t tid = threadIdx.x % NT;
     const uint32_t bar = 1 + grp;     // named barrier of this tile group (0 = __syncthreads)
     const bool init = P.flags & F_INIT;
+    // gather table (leading transposes folded into the first shared-memory read), after the buffers
+    uint16_t *gsm = reinterpret_cast<uint16_t *>(smraw + (size_t)NBUF * (1u << TB) * sizeof(V));
+    if (P.gtab != 0xFFFFu) {
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(P.prm + P.gtab);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(gsm);
+        for (uint32_t i = threadIdx.x; i < NR * NT / 2; i += NT * NG) dst[i] = src[i];
+    }
     if (threadIdx.x == 0) {
         for (int b = 0; b < NBUF; ++b) mbar_init(&mbar[b], NT);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -696,12 +705,17 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
             }
         } else {
             // the tile has landed in shared memory in logical order: read it in the phase-0 layout
-            uint32_t t0 = 0;
+            if (P.gtab != 0xFFFFu) {
 #pragma unroll
-            for (int q = 0; q < NTB; ++q) t0 |= ((tid >> q) & 1u) << P.ph[0].tl[q];
-            t0 = swz(t0) * (uint32_t)sizeof(V);
+                for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + gsm[r * NT + tid]);
+            } else {
+                uint32_t t0 = 0;
 #pragma unroll
-            for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + (t0 ^ P.ph[0].so[r]));
+                for (int q = 0; q < NTB; ++q) t0 |= ((tid >> q) & 1u) << P.ph[0].tl[q];
+                t0 = swz(t0) * (uint32_t)sizeof(V);
+#pragma unroll
+                for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + (t0 ^ P.ph[0].so[r]));
+            }
         }
         if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: release the buffer right away
             named_bar(bar);
@@ -1093,6 +1107,7 @@ struct Built {
     uint8_t pin0[NR];      // absorbed entry permutation of phase 0: register r reads pattern pin0[r]
     uint8_t pout_last[NR]; // absorbed exit permutation of the last phase: register s written as pattern pout[s]
     int h_absorbed = 0;    // H's folded into C_CU records (exactly scaled there)
+    size_t prm_used = 0;   // doubles of P.prm the records use
 };
 
 // parameter doubles a record reads at prm[pi]
@@ -1811,6 +1826,7 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
     std::copy(phases.begin(), phases.end(), P.ph);
     std::copy(recs.begin(), recs.end(), P.g);
     std::copy(prm.begin(), prm.end(), P.prm);
+    B.prm_used = (prm.size() + 1) & ~(size_t)1;   // the gather table starts 16-byte aligned
 }
 
 static int blocks_per_sm(int prec)
@@ -1818,7 +1834,7 @@ static int blocks_per_sm(int prec)
     static int occ[2] = {0, 0};
     int &o = occ[prec == 128 ? 1 : 0];
     if (!o) {
-        size_t smem = (size_t)NBUF * (1 << TB) * (prec == 128 ? 16 : 8);
+        size_t smem = (size_t)NBUF * (1 << TB) * (prec == 128 ? 16 : 8) + NR * NT * 2;
         if (prec == 128) {
             cudaFuncSetAttribute(k_fused<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused<double>, NT * NG, smem);
@@ -1940,6 +1956,46 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 P.gj[j] = o;
                 P.sj[j] = (uint16_t)swz((uint32_t)j << NTB);
             }
+            // Leading transposes (phases whose records were all absorbed, e.g. the error-free Toffoli
+            // ladders of an Adder group) fold into the first shared-memory read: the data movement of
+            // the whole chain is simulated here and the read becomes a gather through a table
+            P.gtab = 0xFFFFu;
+            static const bool no_gather = getenv("TUSQ_NO_GATHER") != nullptr;
+            uint32_t kstar = 0;
+            while (kstar < P.ngate && P.g[kstar].code == C_XPOSE) ++kstar;
+            if (!no_gather && !pending_init && kstar > 0 && B.prm_used + NR * NT / 4 <= (size_t)MAXP) {
+                static uint16_t V[NT][NR], M[1 << TB];
+                auto tt = [&](const Phase &ph, uint32_t t) {
+                    uint32_t x = 0;
+                    for (int j = 0; j < NTB; ++j) x |= ((t >> j) & 1u) << ph.tl[j];
+                    return swz(x);
+                };
+                for (uint32_t t = 0; t < (uint32_t)NT; ++t)
+                    for (int r = 0; r < NR; ++r) V[t][r] = (uint16_t)(tt(P.ph[0], t) ^ P.ph[0].so[r]);
+                uint32_t cur = 0;
+                for (uint32_t k = 0; k < kstar; ++k) {
+                    const Phase &a = P.ph[cur], &b = P.ph[P.g[k].a];
+                    for (uint32_t t = 0; t < (uint32_t)NT; ++t)
+                        for (int r = 0; r < NR; ++r) M[tt(a, t) ^ a.so_out[r]] = V[t][r];
+                    for (uint32_t t = 0; t < (uint32_t)NT; ++t)
+                        for (int r = 0; r < NR; ++r) V[t][r] = M[tt(b, t) ^ b.so[r]];
+                    cur = P.g[k].a;
+                }
+                const uint32_t esz = prec_ == 128 ? 16 : 8;
+                uint16_t *tab = reinterpret_cast<uint16_t *>(P.prm + B.prm_used);
+                for (uint32_t t = 0; t < (uint32_t)NT; ++t)
+                    for (int r = 0; r < NR; ++r) tab[r * NT + t] = (uint16_t)(V[t][r] * esz);
+                P.gtab = (uint16_t)B.prm_used;
+                // phase `cur` becomes phase 0; drop the folded records
+                for (uint32_t k = cur; k < P.nphase; ++k) P.ph[k - cur] = P.ph[k];
+                P.nphase -= cur;
+                for (uint32_t i = kstar; i < P.ngate; ++i) {
+                    P.g[i - kstar] = P.g[i];
+                    if (P.g[i - kstar].code == C_XPOSE) P.g[i - kstar].a = (uint8_t)(P.g[i - kstar].a - cur);
+                }
+                P.ngate -= kstar;
+                if (P.ngate < (uint32_t)MAXG) P.g[P.ngate] = GRec{};
+            }
             P.last_xpose = 0xFFFFu;
             for (uint32_t i = 0; i < P.ngate; ++i)
                 if (P.g[i].code == C_XPOSE) P.last_xpose = (uint16_t)i;
@@ -1968,7 +2024,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         if (!ctx.dry) {
             int bps = blocks_per_sm(prec_);
             uint64_t grid = std::min<uint64_t>((P.ntiles + NG - 1) / NG, (uint64_t)device_sm_count() * bps);
-            size_t smem = (size_t)NBUF * (1 << TB) * (prec_ == 128 ? 16 : 8);
+            size_t smem = (size_t)NBUF * (1 << TB) * (prec_ == 128 ? 16 : 8) + NR * NT * 2;
             // incremental tile bases (deposited steps) and byte offsets for the kernel
             P.outer = ((n_ == 64 ? ~0ull : (1ull << n_) - 1)) & ~B.tile;
             auto pdep = [&](uint64_t x) {
