@@ -983,6 +983,9 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
     // strict: every qubit an op touches (controls, diagonals) must join the tile, so whole runs
     // stay in registers and fold; otherwise they join only while there is room
     const uint64_t low = 7;   // qubits 0,1,2 are always tile qubits
+    // tile qubits a group may claim beyond 0-2 (default all 9; fewer leave fillers 3, 4... in the
+    // tile, i.e. longer contiguous runs per tile row, at the price of more sweeps)
+    static const int hi_cap = getenv("TUSQ_HI_CAP") ? atoi(getenv("TUSQ_HI_CAP")) : TB - 3;
     std::vector<Group> groups;
     Group g;
     uint64_t touched = 0;
@@ -1038,7 +1041,7 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
         // group before the core's first H when the core's qubits would not fit
         if (!g.ops.empty()) {
             const uint64_t cq = core_qubits(oi);
-            if (cq && popc_hi(g.tilemask | cq) > TB - 3) close();
+            if (cq && popc_hi(g.tilemask | cq) > hi_cap) close();
         }
         // requirements of this op on the group's tile set
         const bool xy = (o.kind == X || o.kind == Y);
@@ -1051,7 +1054,7 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
             uint32_t q = __builtin_ctzll(m);
             if (pending[q] >= 0) need |= bit(q);
         }
-        const bool fits = popc_hi(g.tilemask | need) <= TB - 3 && g.ops.size() + 1 < (size_t)MAXG - 8;
+        const bool fits = popc_hi(g.tilemask | need) <= hi_cap && g.ops.size() + 1 < (size_t)MAXG - 8;
         if (!fits) close();
         // re-evaluate after a possible close (pending cleared)
         need = 0;
@@ -1059,7 +1062,7 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
         if (o.kind == CX) need |= bit(o.q1);
         if (strict && !xy) need |= qm;
         // soft: controls / diagonal qubits join the tile while there is room (never close a group)
-        if (!xy && popc_hi(g.tilemask | need | qm) <= TB - 3) need |= qm;
+        if (!xy && popc_hi(g.tilemask | need | qm) <= hi_cap) need |= qm;
         for (uint64_t m = qm; m; m &= m - 1) {
             uint32_t q = __builtin_ctzll(m);
             if (pending[q] >= 0) {
