@@ -69,8 +69,9 @@ enum Code : uint16_t {
     C_CX2 = 123,  // +25c+5t1+t2 (t1 < t2): CX(c->t1) CX(c->t2) as ONE swap pass
     C_CU = 248,   // +6p+j   2x2 on bit p per pattern of the control pair j (Toffoli cores), 32 params
     C_CCX = 278,  // +6p+j   Toffoli on register bits: swap bit p where both controls of pair j are 1
-    C_N = 308,    // number of gate codes
-    C_XPOSE = 308 // transpose registers to phase a
+    C_TDK = 308,  // +r      bit 1 of reg r *= prod_k (pred(q_k) ? e^{i t_k} : 1), a = k count (3a params)
+    C_N = 313,    // number of gate codes
+    C_XPOSE = 313 // transpose registers to phase a
 };
 
 // the j-th (0..5) pair {u < v} of register bits other than p, as a mask (with p): the diagonal of a
@@ -420,6 +421,7 @@ __host__ __device__ constexpr bool code_ok(int C)
     if (C < C_TPH) return (C - C_TX) % 5 < RB;
     if (C == C_TPH) return true;
     if (C < C_CX2) return C - C_DK < NR;
+    if (C >= C_TDK) return (C - C_TDK) < RB;
     if (C >= C_CCX) return hdh_mask((C - C_CCX) / 6, (C - C_CCX) % 6) < NR;
     if (C >= C_CU) return hdh_mask((C - C_CU) / 6, (C - C_CU) % 6) < NR;
     const int c = (C - C_CX2) / 25, t1 = (C - C_CX2) / 5 % 5, t2 = (C - C_CX2) % 5;
@@ -460,6 +462,19 @@ __device__ __forceinline__ void gate_case(V (&a)[NR], const double *p, uint64_t 
 #pragma unroll
             for (int i = 0; i < NR; ++i) cmul_ip(a[i], fr, fi);
         }
+    } else if constexpr (C >= C_TDK) {
+        // a run of controlled phases from outer/thread qubits onto one register bit (QFT ladders):
+        // the per-thread factor is a product of scalars, applied once
+        double fr = 1.0, fi = 0.0;
+        for (uint32_t k = 0; k < ga; ++k) {
+            const double *e = p + 3 * k;
+            if ((lbase >> (uint32_t)e[0]) & 1) {
+                const double nr = fr * e[1] - fi * e[2];
+                fi = fr * e[2] + fi * e[1];
+                fr = nr;
+            }
+        }
+        if (fr != 1.0 || fi != 0.0) g_d1<C - C_TDK, V, R>(a, (R)fr, (R)fi);
     } else if constexpr (C >= C_CCX) {
         constexpr int pb = (C - C_CCX) / 6;
         g_cx<(hdh_mask(pb, (C - C_CCX) % 6) & ~(1 << pb)), pb, V, true>(a);
@@ -493,7 +508,8 @@ __device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const doub
     // fast paths for the two hottest classes (H and diagonal tables: ~2/3 of all records)
     // ordered by frequency in Adder groups: Toffoli swaps, CX, diagonal tables, H, CU, rest
     const int c = g.code;
-    if (c >= C_CCX) dispatch<C_CCX, C_N, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    if (c >= C_TDK) dispatch<C_TDK, C_N, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else if (c >= C_CCX) dispatch<C_CCX, C_TDK, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
     else if (c >= C_CX && c < C_CPH) dispatch<C_CX, C_CPH, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
     else if (c >= C_DK && c < C_DK + NR) dispatch<C_DK, C_DK + NR, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
     else if (c < C_U) dispatch<0, C_U, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
@@ -1114,8 +1130,10 @@ struct Built {
 };
 
 // parameter doubles a record reads at prm[pi]
-static int rec_nparams(uint16_t c)
+static int rec_nparams(const GRec &r)
 {
+    const uint16_t c = r.code;
+    if (c >= C_TDK && c < C_N) return 3 * r.a;
     if (c >= C_U && c < C_X) return 8;
     if (c >= C_D1 && c < C_D2) return 2;
     if (c >= C_D2 && c < C_CX) return 4;
@@ -1132,14 +1150,14 @@ static bool is_perm_rec(uint16_t c)
     if (c >= C_X && c < C_X + 5) return true;
     if (c >= C_CX && c < C_CX + 25) return (c - C_CX) / 5 != (c - C_CX) % 5;
     if (c >= C_CX2 && c < C_CU) return code_ok(c);
-    if (c >= C_CCX && c < C_N) return code_ok(c);
+    if (c >= C_CCX && c < C_TDK) return code_ok(c);
     return false;
 }
 
 static uint32_t perm_apply(uint16_t c, uint32_t r)
 {
     if (c < C_X + 5) return r ^ (1u << (c - C_X));
-    if (c >= C_CCX) {
+    if (c >= C_CCX && c < C_TDK) {
         const int p = (c - C_CCX) / 6;
         const uint32_t cm = (uint32_t)hdh_mask(p, (c - C_CCX) % 6) & ~(1u << p);
         return (r & cm) == cm ? r ^ (1u << p) : r;
@@ -1513,6 +1531,43 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         for (auto &ph : phases) { ph.g0 = newidx[ph.g0]; ph.g1 = newidx[ph.g1]; }
         recs.swap(m);
     }
+    // Runs of controlled phases from non-register qubits onto the same register bit (C_TD1: the CP
+    // ladders of a QFT, ~30 per H at 34 qubits) merge into one C_TDK record: the kernel multiplies
+    // the per-thread scalar factors first and touches the amplitudes once.
+    {
+        static const bool no_tdk = getenv("TUSQ_NO_TDK") != nullptr;
+        std::vector<GRec> m;
+        m.reserve(recs.size());
+        std::vector<uint16_t> newidx(recs.size() + 1);
+        for (size_t j = 0; j < recs.size(); ++j) {
+            newidx[j] = (uint16_t)m.size();
+            const uint16_t c0 = recs[j].code;
+            size_t k = j;
+            if (!no_tdk && c0 >= C_TD1 && c0 < C_TD1 + RB)
+                while (k < recs.size() && recs[k].code == c0 && k - j < 255) ++k;
+            if (k - j >= 2) {
+                GRec r;
+                memset(&r, 0, sizeof(r));
+                r.code = (uint16_t)(C_TDK + (c0 - C_TD1));
+                r.a = (uint8_t)(k - j);
+                r.pi = (uint16_t)prm.size();
+                for (size_t q = j; q < k; ++q) {
+                    const double e0 = (double)recs[q].a, e1 = prm[recs[q].pi], e2 = prm[recs[q].pi + 1];
+                    prm.push_back(e0);
+                    prm.push_back(e1);
+                    prm.push_back(e2);
+                    newidx[q] = (uint16_t)m.size();
+                }
+                m.push_back(r);
+                j = k - 1;
+                continue;
+            }
+            m.push_back(recs[j]);
+        }
+        newidx[recs.size()] = (uint16_t)m.size();
+        for (auto &ph : phases) { ph.g0 = newidx[ph.g0]; ph.g1 = newidx[ph.g1]; }
+        recs.swap(m);
+    }
     // Toffoli cores: H(t) DK(a, b, t) H(t) [DK(subset of a, b)] is, per pattern of the controls
     // (a, b), a 2x2 matrix on t -- ONE controlled-2x2 record (C_CU) replaces 3-4 records.  The host
     // multiplies the blocks out exactly as the gates define them (the two H's included, so the
@@ -1775,7 +1830,7 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         std::vector<double> used;
         used.reserve(prm.size());
         for (auto &r : recs) {
-            const int np = rec_nparams(r.code);
+            const int np = rec_nparams(r);
             if (!np) continue;
             const uint16_t at = (uint16_t)used.size();
             used.insert(used.end(), prm.begin() + r.pi, prm.begin() + r.pi + np);
@@ -2069,7 +2124,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                         const uint16_t c = P.g[i].code;
                         int k = c < C_U ? 0 : (c >= C_DK && c < C_CX2) ? 1 : ((c >= C_CX && c < C_CPH) || (c >= C_CX2 && c < C_CU)) ? 2
                                 : (c >= C_D1 && c < C_CX) ? 3 : c == C_XPOSE ? 4 : (c >= C_X && c < C_D1) ? 5
-                                : (c >= C_TX && c <= C_TPH) ? 6 : (c >= C_CU && c < C_CCX) ? 8 : (c >= C_CCX && c < C_N) ? 2 : 7;
+                                : (c >= C_TX && c <= C_TPH) ? 6 : (c >= C_CU && c < C_CCX) ? 8 : (c >= C_CCX && c < C_TDK) ? 2 : (c >= C_TDK && c < C_N) ? 3 : 7;
                         cnt[k]++;
                     }
                     snprintf(tag, sizeof(tag), "ops %zu recs %u ph %u init %d tile %#llx H%d DK%d CX%d D%d XP%d XY%d T%d O%d CU%d",
