@@ -69,7 +69,7 @@ enum Code : uint16_t {
     C_CX2 = 123,  // +25c+5t1+t2 (t1 < t2): CX(c->t1) CX(c->t2) as ONE swap pass
     C_CU = 248,   // +6p+j   2x2 on bit p per pattern of the control pair j (Toffoli cores), 32 params
     C_CCX = 278,  // +6p+j   Toffoli on register bits: swap bit p where both controls of pair j are 1
-    C_TDK = 308,  // +r      bit 1 of reg r *= e^{i sum_k pred(q_k) t_k}, a = k count (2a params: q_k, t_k)
+    C_TDK = 308,  // +r      bit 1 of reg r *= prod_k (pred(q_k) ? e^{i t_k} : 1), a = k count (3a params)
     C_N = 313,    // number of gate codes
     C_XPOSE = 313 // transpose registers to phase a
 };
@@ -464,17 +464,17 @@ __device__ __forceinline__ void gate_case(V (&a)[NR], const double *p, uint64_t 
         }
     } else if constexpr (C >= C_TDK) {
         // a run of controlled phases from outer/thread qubits onto one register bit (QFT ladders):
-        // the per-thread angle is a predicated sum, turned into one phase and applied once
-        double th = 0.0;
+        // the per-thread factor is a product of scalars, applied once
+        double fr = 1.0, fi = 0.0;
         for (uint32_t k = 0; k < ga; ++k) {
-            const double *e = p + 2 * k;
-            th += ((lbase >> (uint32_t)e[0]) & 1) ? e[1] : 0.0;
+            const double *e = p + 3 * k;
+            if ((lbase >> (uint32_t)e[0]) & 1) {
+                const double nr = fr * e[1] - fi * e[2];
+                fi = fr * e[2] + fi * e[1];
+                fr = nr;
+            }
         }
-        if (th != 0.0) {
-            double sn, cs;
-            sincos(th, &sn, &cs);
-            g_d1<C - C_TDK, V, R>(a, (R)cs, (R)sn);
-        }
+        if (fr != 1.0 || fi != 0.0) g_d1<C - C_TDK, V, R>(a, (R)fr, (R)fi);
     } else if constexpr (C >= C_CCX) {
         constexpr int pb = (C - C_CCX) / 6;
         g_cx<(hdh_mask(pb, (C - C_CCX) % 6) & ~(1 << pb)), pb, V, true>(a);
@@ -1133,7 +1133,7 @@ struct Built {
 static int rec_nparams(const GRec &r)
 {
     const uint16_t c = r.code;
-    if (c >= C_TDK && c < C_N) return 2 * r.a;
+    if (c >= C_TDK && c < C_N) return 3 * r.a;
     if (c >= C_U && c < C_X) return 8;
     if (c >= C_D1 && c < C_D2) return 2;
     if (c >= C_D2 && c < C_CX) return 4;
@@ -1552,9 +1552,10 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                 r.a = (uint8_t)(k - j);
                 r.pi = (uint16_t)prm.size();
                 for (size_t q = j; q < k; ++q) {
-                    // the phase (cos t, sin t) of a CP (or -1 of a CZ) as its angle t
-                    prm.push_back((double)recs[q].a);
-                    prm.push_back(atan2(prm[recs[q].pi + 1], prm[recs[q].pi]));
+                    const double e0 = (double)recs[q].a, e1 = prm[recs[q].pi], e2 = prm[recs[q].pi + 1];
+                    prm.push_back(e0);
+                    prm.push_back(e1);
+                    prm.push_back(e2);
                     newidx[q] = (uint16_t)m.size();
                 }
                 m.push_back(r);
