@@ -31,6 +31,12 @@
  *     thread) says why.
  *   - There is no CPU fallback: every device step runs in this library's
  *     sm_100a kernels; calls that need a GPU fail with TUSQ_ERR_CUDA without one.
+ *   - Thread safety: every call is reentrant.  Trees are immutable after
+ *     tusq_build_error_tree and may be shared by threads (e.g. one host thread per
+ *     GPU); a communicator and a caller-owned state buffer must be used by one
+ *     call at a time.  The library keeps no mutable process-global state besides
+ *     lazily initialised, thread-safe caches (device attributes, the NCCL entry
+ *     points).
  */
 #ifndef TUSQ_ABI_H_
 #define TUSQ_ABI_H_
@@ -123,10 +129,17 @@ typedef struct {
     uint64_t leaf_end;          /*   leaf_end = 0 means all leaves */
     uint64_t reanchor_budget;   /* re-anchor (reset + replay) once this many gate applications have
                                    accumulated since the last anchor; 0 = default (1e6 c128, 2e4 c64) */
-    uint32_t fuse_qubits;       /* tile qubits of the fused kernel; 0 = default (12) */
+    uint32_t fuse_qubits;       /* tile qubits of the fused kernel: 0 or 12 (the only tile this build
+                                   compiles); anything else -> TUSQ_ERR_UNSUPPORTED */
     uint32_t _pad;
     double   edge_eps;          /* edge-draw window (0 = 1e-9 for c128, 1e-5 for c64) */
-    tusq_comm *comm;            /* TUSQ_MODE_SHARDED: the communicator (NULL otherwise) */
+    tusq_comm *comm;            /* TUSQ_MODE_SHARDED: the communicator (required).
+                                   TUSQ_MODE_REPLICA: NULL (single process), or an NCCL communicator
+                                   (tusq_comm_init) of the replica ranks: this rank runs its leaf range
+                                   (leaf_begin = leaf_end = 0 -> its tusq_tree_partition range) and the
+                                   slot arrays of all ranks are summed with ncclAllReduce on the device
+                                   (they are disjoint, so the sum is exact); out_slots then receives all
+                                   S1 slots on every rank.  A local communicator is rejected here. */
 } tusq_exec;
 
 typedef struct {
@@ -145,6 +158,13 @@ typedef struct {
     double   gate_kernel_bytes;     /* algorithmic HBM bytes of those launches */
     uint64_t fused_launches;        /* K5 launches among `launches` */
     uint64_t exchanges;             /* sharded mode: global<->local qubit swaps (NCCL send/recv of half shards) */
+    double   sample_kernel_seconds; /* TUSQ_EXEC_PROFILE: summed CUDA-event durations of the sampler (K6) launches */
+    double   device_seconds;        /* CUDA-event time from the first launch of the call to its last one */
+    double   reduce_seconds;        /* replica mode with comm: CUDA-event time of the slot all-reduce */
+    double   h2d_bytes;             /* host -> device bytes of the call (kernel parameter blocks, draw tables) */
+    double   d2h_bytes;             /* device -> host bytes of the call (slots, counters) */
+    uint64_t sampled_vectors;       /* state vectors sampled (leaves that share a vector under a terminal
+                                       relabel count once) */
 } tusq_run_stats;
 
 /* ECM + tree.  ops: n_ops gates (host).  seed keys every Philox stream.
@@ -169,7 +189,10 @@ tusq_status tusq_tree_leaf(const tusq_tree *tree, uint64_t leaf, uint64_t *count
                            uint32_t *triples, uint32_t *inout_n);
 
 /* Contiguous DFS leaf ranges for nranks replicas balanced by the host cost model
- * (SURVEY 8(e)): bounds[r]..bounds[r+1] for r < nranks (nranks + 1 entries). */
+ * (SURVEY 8(e)): bounds[r]..bounds[r+1] for r < nranks (nranks + 1 entries).  The model replays
+ * the scheduler of tusq_run_tree for `precision` (64 or 128): hybrid reset-vs-uncompute per
+ * transition, plus the precision's re-anchor budget (1e6 gate applications c128, 2e4 c64), in
+ * gate applications. */
 tusq_status tusq_tree_partition(const tusq_tree *tree, uint32_t nranks, uint32_t precision, uint64_t *bounds);
 
 void tusq_tree_free(tusq_tree *tree);

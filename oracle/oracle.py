@@ -63,6 +63,9 @@ def lib():
         L.or_apply_gate.argtypes = [dp, C.c_uint32, C.c_void_p, C.c_int]
         L.or_replay.argtypes = [C.c_uint32, C.c_void_p, C.c_uint64, u32p, C.c_uint32, C.c_int, C.c_int, dp]
         L.or_replay_leaf.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, dp]
+        L.or_replay_leaf_core.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, dp]
+        L.or_terminal_mask.restype = C.c_uint64
+        L.or_terminal_mask.argtypes = [C.c_void_p, C.c_uint64]
         L.or_sample_state.argtypes = [dp, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
                                       u64p, C.POINTER(C.c_uint8)]
         L.or_run.argtypes = [C.c_void_p, C.c_void_p, C.c_double, u64p, C.POINTER(C.c_uint8)]
@@ -219,9 +222,23 @@ class Tree:
         assert rc == 0
         return st
 
-    def sample_leaf(self, state, l: int, edge_eps=1e-9):
+    def replay_leaf_core(self, l: int) -> np.ndarray:
+        """The state leaf l is sampled from: its triples before the readout only (reading #7)."""
+        st = np.zeros(1 << self.n, dtype=np.complex128)
+        rc = lib().or_replay_leaf_core(self.h, self._ops.ctypes.data, l,
+                                       st.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)))
+        assert rc == 0
+        return st
+
+    def terminal_mask(self, l: int) -> int:
+        """Readout flips of leaf l (its terminal X triples) as a bit mask."""
+        return int(lib().or_terminal_mask(self.h, l))
+
+    def sample_leaf(self, core_state, l: int, edge_eps=1e-9):
+        """Leaf l's draws from its core state (replay_leaf_core), flipped by its terminal mask."""
         _, cnt, _ = self.leaf(l)
-        return sample_state(state, self.n, self.seed, l, cnt, edge_eps)
+        k, edge = sample_state(core_state, self.n, self.seed, l, cnt, edge_eps)
+        return k ^ np.uint64(self.terminal_mask(l)), edge
 
     def run(self, edge_eps=1e-9):
         S = self.stats()["S1"]

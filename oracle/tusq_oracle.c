@@ -761,6 +761,34 @@ int or_replay_leaf(const void *p, const or_op *ops, uint64_t leaf, double *state
     return or_replay(t->n_qubits, ops, t->n_ops, t->leaves[leaf].tr, t->leaves[leaf].n, 1, 1, state);
 }
 
+/*
+ * The state a leaf is SAMPLED from (reading #7): the leaf's triples before the readout
+ * (pos < L) only.  Its terminal triples (pos = L: X flips of the readout, "measurement noise
+ * is modeled as stochastic injection of the X gate") do not touch the amplitudes; they flip
+ * bits of every bitstring drawn for the leaf (or_terminal_mask).  Applying X before an ideal
+ * measurement and flipping the measured bit are the same channel on the outcome distribution.
+ */
+int or_replay_leaf_core(const void *p, const or_op *ops, uint64_t leaf, double *state)
+{
+    const or_tree *t = (const or_tree *)p;
+    if (leaf >= t->n_leaves) return 1;
+    uint32_t m = 0;   /* triples are sorted by pos: the core is a prefix */
+    while (m < t->leaves[leaf].n && t->leaves[leaf].tr[3 * m] < t->n_ops) m++;
+    return or_replay(t->n_qubits, ops, t->n_ops, t->leaves[leaf].tr, m, 1, 1, state);
+}
+
+uint64_t or_terminal_mask(const void *p, uint64_t leaf)
+{
+    const or_tree *t = (const or_tree *)p;
+    uint64_t mask = 0;
+    if (leaf >= t->n_leaves) return 0;
+    for (uint32_t i = 0; i < t->leaves[leaf].n; i++) {
+        const uint32_t *x = t->leaves[leaf].tr + 3 * i;
+        if (x[0] == t->n_ops && (x[2] == PAULI_X || x[2] == PAULI_Y)) mask ^= (uint64_t)1 << x[1];
+    }
+    return mask;
+}
+
 /* ===================================================================== sampling
  * p_k = re*re + im*im (no FMA).  C(k) is a compensated (Neumaier) sequential
  * sum, T = C(N-1).  Draw j of leaf l: Philox counter (j_lo, l_lo, l_hi,
@@ -826,7 +854,8 @@ int or_sample_state(const double *state, uint32_t n, uint64_t seed, uint64_t lea
     return 0;
 }
 
-/* Full oracle run: every leaf replayed from |0..0> and sampled into its slots. */
+/* Full oracle run: every leaf's core replayed from |0..0>, sampled into its slots, and the
+ * drawn bitstrings flipped by its terminal X mask (reading #7). */
 int or_run(const void *p, const or_op *ops, double edge_eps, uint64_t *slots, uint8_t *edge)
 {
     const or_tree *t = (const or_tree *)p;
@@ -834,8 +863,11 @@ int or_run(const void *p, const or_op *ops, double edge_eps, uint64_t *slots, ui
     double *st = (double *)malloc(sizeof(double) * 2 * ((size_t)1 << n));
     if (!st) return 3;
     for (uint64_t l = 0; l < t->n_leaves; l++) {
-        or_replay_leaf(p, ops, l, st);
-        or_sample_state(st, n, t->seed, l, t->leaves[l].count, edge_eps, slots + t->offsets[l], edge + t->offsets[l]);
+        or_replay_leaf_core(p, ops, l, st);
+        uint64_t *out = slots + t->offsets[l];
+        or_sample_state(st, n, t->seed, l, t->leaves[l].count, edge_eps, out, edge + t->offsets[l]);
+        uint64_t mask = or_terminal_mask(p, l);
+        for (uint64_t j = 0; j < t->leaves[l].count; j++) out[j] ^= mask;
     }
     free(st);
     return 0;

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -44,18 +45,26 @@ static tusq_status validate_ops(uint32_t n, const tusq_op *ops, uint64_t L)
 
 static bool prec_ok(uint32_t p) { return p == 128 || p == 64; }
 static uint32_t block_bits_for(uint32_t n) { return n < 12 ? n : 12; }
+// the 2^n state's byte count must fit 63 bits (n <= 58 c128, 59 c64: far above any device)
+static bool state_fits(uint32_t n, int prec) { return n + (prec == 128 ? 4u : 3u) <= 62u; }
 
-// Host cost model of one transition (gate applications): hybrid min(uncompute, reset).
-static uint64_t transition_cost(const tusq_tree &t, const Leaf *prev, const Leaf &l, bool hybrid, bool fold)
+// Stream-ordered device scratch from the device's default memory pool.  The pool keeps freed
+// memory (release threshold raised once per device), so per-call scratch costs no cudaMalloc /
+// cudaFree round trip and no device-wide synchronization.
+static cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st)
 {
-    uint64_t idx;
-    double re, im;
-    Cursor cf = fold ? fold_prefix(t, l, &idx, &re, &im) : Cursor{0, 0};
-    uint64_t reset = suffix_len(t, l, cf);
-    if (!prev) return reset;
-    Cursor c = common_prefix(t, *prev, l);
-    uint64_t unc = suffix_len(t, *prev, c) + suffix_len(t, l, c);
-    return hybrid ? std::min(unc, reset) : unc;
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::call_once(once[dev & 63], [dev]() {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = 1ull << 30;   // keep up to 1 GiB of freed scratch
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+    return cudaMallocAsync(p, bytes, st);
 }
 
 }  // namespace tq
@@ -148,12 +157,33 @@ void tusq_tree_free(tusq_tree *t) { delete t; }
 
 tusq_status tusq_tree_partition(const tusq_tree *t, uint32_t nranks, uint32_t precision, uint64_t *bounds)
 {
-    (void)precision;
     if (!t || !bounds || nranks == 0) return fail(TUSQ_ERR_INVALID_ARG, "bad argument");
+    if (!prec_ok(precision)) return fail(TUSQ_ERR_INVALID_ARG, "precision must be 128 or 64");
     const uint64_t nl = t->leaves.size();
+    const uint32_t L = (uint32_t)t->gates.size();
+    const uint64_t budget = precision == 128 ? 1000000ull : 20000ull;
+    // replay the scheduler of tusq_run_tree on the executed (core) leaves: hybrid reset vs
+    // uncompute, and a forced re-anchor whenever the precision's budget would be exceeded
     std::vector<double> cum(nl + 1, 0.0);
-    for (uint64_t i = 0; i < nl; ++i)
-        cum[i + 1] = cum[i] + (double)transition_cost(*t, i ? &t->leaves[i - 1] : nullptr, t->leaves[i], true, true);
+    uint64_t since = 0;
+    Leaf prev;
+    for (uint64_t i = 0; i < nl; ++i) {
+        const Leaf cur = core_of(t->leaves[i], L, nullptr);
+        uint64_t idx;
+        double re, im;
+        const uint64_t reset = suffix_len(*t, cur, fold_prefix(*t, cur, &idx, &re, &im));
+        uint64_t cost = reset;
+        if (i) {
+            const Cursor c = common_prefix(*t, prev, cur);
+            const uint64_t unc = suffix_len(*t, prev, c) + suffix_len(*t, cur, c);
+            if (unc <= reset && since + unc <= budget) { cost = unc; since += unc; }
+            else since = reset;
+        } else {
+            since = reset;
+        }
+        cum[i + 1] = cum[i] + (double)cost;
+        prev = cur;
+    }
     bounds[0] = 0;
     uint64_t i = 0;
     for (uint32_t r = 1; r < nranks; ++r) {
@@ -168,7 +198,7 @@ tusq_status tusq_tree_partition(const tusq_tree *t, uint32_t nranks, uint32_t pr
 tusq_status tusq_init_basis(void *d_state, uint32_t n, uint32_t precision, uint64_t index, double re, double im,
                             void *stream)
 {
-    if (!d_state || n == 0 || n > 62 || !prec_ok(precision) || index >= (1ull << n))
+    if (!d_state || n == 0 || !prec_ok(precision) || !state_fits(n, (int)precision) || index >= (1ull << n))
         return fail(TUSQ_ERR_INVALID_ARG, "bad argument");
     launch_init_basis(d_state, n, (int)precision, index, re, im, (cudaStream_t)stream);
     TQ_CUDA(cudaGetLastError());
@@ -181,6 +211,7 @@ tusq_status tusq_apply_ops(void *d_state, uint32_t n, uint32_t precision, const 
     if (!d_state || !prec_ok(precision)) return fail(TUSQ_ERR_INVALID_ARG, "bad argument");
     tusq_status s = validate_ops(n, ops, L);
     if (s) return s;
+    if (!state_fits(n, (int)precision)) return fail(TUSQ_ERR_CAPACITY, "2^n state too large");
     std::vector<Op> v(L);
     for (uint64_t i = 0; i < L; ++i) v[i] = Op{ops[i].kind, ops[i].q0, ops[i].q1, ops[i].theta};
     if (flags & TUSQ_APPLY_INVERSE) {
@@ -193,7 +224,7 @@ tusq_status tusq_apply_ops(void *d_state, uint32_t n, uint32_t precision, const 
     Ctx ctx;
     ctx.psi = d_state; ctx.n = n; ctx.prec = (int)precision; ctx.st = (cudaStream_t)stream; ctx.stats = &stats;
     ctx.dry = (flags & TUSQ_APPLY_PLAN_ONLY) != 0;
-    FusedPlanner planner(n, (int)precision, 0);
+    FusedPlanner planner(n, (int)precision);
     try {
         if (!(flags & TUSQ_APPLY_UNFUSED) && planner.enabled()) {
             planner.execute(v, ctx);
@@ -211,23 +242,24 @@ tusq_status tusq_apply_ops(void *d_state, uint32_t n, uint32_t precision, const 
 tusq_status tusq_sample(const void *d_state, uint32_t n, uint32_t precision, uint64_t n_draws, uint64_t seed,
                         uint64_t leaf, uint64_t *d_out, void *stream)
 {
-    if (!d_state || !d_out || n == 0 || n > 62 || !prec_ok(precision)) return fail(TUSQ_ERR_INVALID_ARG, "bad argument");
+    if (!d_state || !d_out || n == 0 || !prec_ok(precision) || !state_fits(n, (int)precision))
+        return fail(TUSQ_ERR_INVALID_ARG, "bad argument");
     if (!n_draws) return TUSQ_OK;
     cudaStream_t st = (cudaStream_t)stream;
     uint32_t bb = block_bits_for(n);
     uint64_t nb = 1ull << (n - bb);
-    double *d_blocks = nullptr;
-    uint32_t *d_edges = nullptr;
-    TQ_CUDA(cudaMallocAsync((void **)&d_blocks, (2 * nb + 16) * sizeof(double), st));
-    TQ_CUDA(cudaMallocAsync((void **)&d_edges, sizeof(uint32_t), st));
+    void *scr = nullptr;
+    const size_t nblk = 2 * nb + 16;
+    TQ_CUDA(scratch_alloc(&scr, nblk * sizeof(double) + 16, st));
+    double *d_blocks = (double *)scr;
+    uint32_t *d_edges = (uint32_t *)(d_blocks + nblk);
     TQ_CUDA(cudaMemsetAsync(d_edges, 0, sizeof(uint32_t), st));
     launch_block_sums(d_state, n, (int)precision, bb, d_blocks, st);
     launch_scan_blocks(d_blocks, d_blocks + nb, nb, 0, st);
-    launch_draws(d_state, n, (int)precision, bb, d_blocks, d_blocks + nb, n_draws, seed, leaf, 1e-9, 0, d_out,
-                 d_edges, st);
+    launch_draws(d_state, n, (int)precision, bb, d_blocks, d_blocks + nb, n_draws, seed, leaf, nullptr, 0, 0, 1e-9, 0,
+                 d_out, d_edges, st);
     TQ_CUDA(cudaGetLastError());
-    TQ_CUDA(cudaFreeAsync(d_blocks, st));
-    TQ_CUDA(cudaFreeAsync(d_edges, st));
+    TQ_CUDA(cudaFreeAsync(scr, st));
     return TUSQ_OK;
 }
 
@@ -236,6 +268,9 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     auto t0 = std::chrono::steady_clock::now();
     if (!t || !ex) return fail(TUSQ_ERR_INVALID_ARG, "NULL argument");
     if (!prec_ok(ex->precision)) return fail(TUSQ_ERR_INVALID_ARG, "precision must be 128 or 64");
+    if (ex->fuse_qubits != 0 && ex->fuse_qubits != 12)
+        return fail(TUSQ_ERR_UNSUPPORTED, "fuse_qubits: this build compiles 12-qubit tiles only (0 or 12)");
+    if (!state_fits(t->n, (int)ex->precision)) return fail(TUSQ_ERR_CAPACITY, "2^n state too large");
     if (ex->mode == TUSQ_MODE_SHARDED) {
         try {
             return run_tree_sharded(t, ex, out_slots, stats_out);
@@ -248,11 +283,26 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     const bool sample = !(ex->flags & TUSQ_EXEC_NO_SAMPLE);
     if (sample && !dry && !out_slots) return fail(TUSQ_ERR_INVALID_ARG, "out_slots is NULL");
     const uint32_t n = t->n;
+    const uint32_t L = (uint32_t)t->gates.size();
     const int prec = (int)ex->precision;
     const uint64_t amp_bytes = prec == 128 ? 16 : 8;
     const uint64_t need = amp_bytes << n;
     const uint64_t nl = t->leaves.size();
-    const uint64_t lb = ex->leaf_begin, le = ex->leaf_end ? ex->leaf_end : nl;
+    tusq_comm *comm = ex->comm;
+    int crank = 0, cranks = 1;
+    if (comm) {
+        if (comm_is_local(comm)) return fail(TUSQ_ERR_INVALID_ARG, "replica mode: a local communicator has no ranks to reduce over");
+        crank = comm_rank(comm);
+        cranks = comm_nranks(comm);
+    }
+    uint64_t lb = ex->leaf_begin, le = ex->leaf_end ? ex->leaf_end : nl;
+    if (comm && ex->leaf_begin == 0 && ex->leaf_end == 0) {   // this rank's cost-balanced range
+        std::vector<uint64_t> bounds(cranks + 1);
+        tusq_status ps = tusq_tree_partition(t, (uint32_t)cranks, ex->precision, bounds.data());
+        if (ps) return ps;
+        lb = bounds[crank];
+        le = bounds[crank + 1];
+    }
     if (lb > le || le > nl) return fail(TUSQ_ERR_INVALID_ARG, "leaf range out of bounds");
     if (!dry && ex->device >= 0) TQ_CUDA(cudaSetDevice(ex->device));
     cudaStream_t st = (cudaStream_t)ex->stream;
@@ -268,19 +318,52 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
         own_state = true;
     }
     tusq_run_stats stats{};
-    const uint64_t off0 = lb < le ? t->leaves[lb].offset : 0;
-    const uint64_t off1 = lb < le ? t->leaves[le - 1].offset + t->leaves[le - 1].count : 0;
-    uint64_t *d_slots = nullptr;
-    double *d_blocks = nullptr;
-    uint32_t *d_edges = nullptr;
+    // slot window written by this call: the range's shots, or all S1 slots when reduced over ranks
+    const uint64_t off0 = comm ? 0 : (lb < le ? t->leaves[lb].offset : 0);
+    const uint64_t off1 = comm ? t->shots : (lb < le ? t->leaves[le - 1].offset + t->leaves[le - 1].count : 0);
     const uint32_t bb = block_bits_for(n);
     const uint64_t nb = 1ull << (n - bb);
+
+    // ---- executed (core) leaves and sampling groups: consecutive leaves with the same core share
+    // one state vector; their draws run in one launch with per-leaf readout masks (reading #7)
+    std::vector<Leaf> core(le - lb);
+    std::vector<uint64_t> tmask(le - lb, 0);
+    for (uint64_t li = lb; li < le; ++li) core[li - lb] = core_of(t->leaves[li], L, &tmask[li - lb]);
+    Leaf prev_core;
+    const bool cont = (ex->flags & TUSQ_EXEC_CONTINUE) && lb > 0;
+    if (cont) prev_core = core_of(t->leaves[lb - 1], L, nullptr);
+    struct SGroup { uint64_t l0, l1, tab; };   // leaves [l0, l1), table offset (u64 words), 0 = none
+    std::vector<SGroup> groups;
+    std::vector<uint64_t> htab;
+    for (uint64_t i = 0; i < core.size();) {
+        uint64_t j = i + 1;
+        while (j < core.size() && same_core(core[j], core[i])) ++j;
+        SGroup g{lb + i, lb + j, 0};
+        if (j - i > 1) {
+            g.tab = htab.size() + 1;   // +1: 0 means "no table"
+            for (uint64_t k = i; k <= j; ++k)
+                htab.push_back(k < j ? t->leaves[lb + k].offset - t->leaves[lb + i].offset
+                                     : t->leaves[lb + j - 1].offset + t->leaves[lb + j - 1].count - t->leaves[lb + i].offset);
+            for (uint64_t k = i; k < j; ++k) htab.push_back(tmask[k]);
+        }
+        groups.push_back(g);
+        i = j;
+    }
+
+    // ---- device scratch: slots, block sums + prefix, edge counter, group tables
+    void *scr = nullptr;
+    const size_t nslots = std::max<uint64_t>(1, off1 - off0);
+    const size_t nblk = 2 * nb + 16;
+    const size_t scr_bytes = (nslots + nblk + htab.size() + 2) * 8;
+    uint64_t *d_slots = nullptr, *d_tab = nullptr;
+    double *d_blocks = nullptr;
+    uint32_t *d_edges = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     GateTimer timer(!dry && (ex->flags & TUSQ_EXEC_PROFILE));
     auto cleanup = [&]() {
-        if (d_slots) cudaFree(d_slots);
-        if (d_blocks) cudaFree(d_blocks);
-        if (d_edges) cudaFree(d_edges);
-        if (own_state) cudaFree(psi);
+        if (scr) cudaFreeAsync(scr, st);
+        if (own_state) { cudaStreamSynchronize(st); cudaFree(psi); }
+        for (auto &e : ev) if (e) cudaEventDestroy(e);
     };
 #define TQ_RUN_CUDA(call)                                                                            \
     do {                                                                                             \
@@ -288,16 +371,24 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
         if (e_ != cudaSuccess) { cleanup(); return fail(TUSQ_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); } \
     } while (0)
     if (!dry) {
-        TQ_RUN_CUDA(cudaMalloc((void **)&d_slots, std::max<uint64_t>(1, off1 - off0) * sizeof(uint64_t)));
-        TQ_RUN_CUDA(cudaMalloc((void **)&d_blocks, (2 * nb + 16) * sizeof(double)));
-        TQ_RUN_CUDA(cudaMalloc((void **)&d_edges, sizeof(uint32_t)));
+        for (auto &e : ev) TQ_RUN_CUDA(cudaEventCreate(&e));
+        TQ_RUN_CUDA(cudaEventRecord(ev[0], st));
+        TQ_RUN_CUDA(scratch_alloc(&scr, scr_bytes, st));
+        d_slots = (uint64_t *)scr;
+        d_blocks = (double *)(d_slots + nslots);
+        d_tab = (uint64_t *)(d_blocks + nblk);
+        d_edges = (uint32_t *)(d_tab + htab.size());
+        if (comm) TQ_RUN_CUDA(cudaMemsetAsync(d_slots, 0, nslots * sizeof(uint64_t), st));
         TQ_RUN_CUDA(cudaMemsetAsync(d_edges, 0, sizeof(uint32_t), st));
+        if (!htab.empty())
+            TQ_RUN_CUDA(cudaMemcpyAsync(d_tab, htab.data(), htab.size() * 8, cudaMemcpyHostToDevice, st));
     }
+    stats.h2d_bytes += (double)htab.size() * 8;
     const bool hybrid = !(ex->flags & TUSQ_EXEC_NO_RESET);
     const bool fold = !(ex->flags & TUSQ_EXEC_NO_FOLD);
     const uint64_t budget = ex->reanchor_budget ? ex->reanchor_budget : (prec == 128 ? 1000000ull : 20000ull);
     const double eps = ex->edge_eps > 0 ? ex->edge_eps : (prec == 128 ? 1e-9 : 1e-5);
-    FusedPlanner planner(n, prec, ex->fuse_qubits);
+    FusedPlanner planner(n, prec);
     const bool fuse = !(ex->flags & TUSQ_EXEC_NO_FUSE) && planner.enabled();
     Ctx ctx;
     ctx.psi = psi; ctx.n = n; ctx.prec = prec; ctx.st = st; ctx.dry = dry; ctx.stats = &stats;
@@ -307,10 +398,10 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     uint64_t since_anchor = 0;
     bool phys_sums_valid = false;
     try {
-        for (uint64_t li = lb; li < le; ++li) {
-            const Leaf &l = t->leaves[li];
-            const Leaf *prev = li > lb ? &t->leaves[li - 1]
-                               : ((ex->flags & TUSQ_EXEC_CONTINUE) && lb > 0) ? &t->leaves[lb - 1] : nullptr;
+        for (const SGroup &g : groups) {
+            // ---- transition to the group's core (uncompute to the divergence slot, then forward)
+            const Leaf &l = core[g.l0 - lb];
+            const Leaf *prev = g.l0 > lb ? &core[g.l0 - lb - 1] : (cont ? &prev_core : nullptr);
             ops.clear();
             InitState init{0, 1.0, 0.0};
             Cursor cf = fold ? fold_prefix(*t, l, &init.index, &init.re, &init.im) : Cursor{0, 0};
@@ -334,15 +425,19 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
             }
             stats.gate_apps += ops.size();
             const uint64_t sweeps_before = stats.sweeps;
+            uint64_t draws = 0;
+            for (uint64_t li = g.l0; li < g.l1; ++li) draws += t->leaves[li].count;
             bool sums = false;
-            const bool want_sums = sample && l.count && n >= 12;
+            const bool want_sums = sample && draws && n >= 12;
             if (fuse) {
                 // (plan-only runs pass a placeholder pointer: nothing is launched)
                 double *sums_dst = want_sums ? (dry ? reinterpret_cast<double *>(16) : d_blocks) : nullptr;
                 planner.execute_ex(ops, ctx, reset ? &init : nullptr, sums_dst, &sums);
             } else {
                 if (reset) {
+                    if (ctx.timer) ctx.timer->begin(st);
                     double b = dry ? (double)need : launch_init_basis(psi, n, prec, init.index, init.re, init.im, st);
+                    if (ctx.timer) ctx.timer->end(st, b);
                     stats.launches++;
                     stats.hbm_bytes += b;
                 }
@@ -352,24 +447,31 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
             // relabelled (pending X mask), recomputed when the state changed without an epilogue
             if (sums) phys_sums_valid = true;
             else if (reset || stats.sweeps != sweeps_before) phys_sums_valid = false;
-            if (sample && l.count) {
+            // ---- sampling: one CDF, the draws of every leaf of the group in one launch
+            if (sample && draws) {
                 const uint64_t xm = fuse ? planner.xmask() : 0;
+                if (ctx.timer) ctx.timer->begin(st);
                 if (!phys_sums_valid) {
                     stats.sample_bytes += dry ? (double)need : launch_block_sums(psi, n, prec, bb, d_blocks, st);
                     stats.launches++;
                     phys_sums_valid = true;
                 }
+                const Leaf &l0 = t->leaves[g.l0];
                 if (!dry) {
                     launch_scan_blocks(d_blocks, d_blocks + nb, nb, xm >> bb, st);
-                    stats.sample_bytes += launch_draws(psi, n, prec, bb, d_blocks, d_blocks + nb, l.count, t->seed,
-                                                       li, eps, xm, d_slots + (l.offset - off0), d_edges, st);
+                    stats.sample_bytes += launch_draws(psi, n, prec, bb, d_blocks, d_blocks + nb, draws, t->seed, g.l0,
+                                                       g.tab ? d_tab + (g.tab - 1) : nullptr, (uint32_t)(g.l1 - g.l0),
+                                                       tmask[g.l0 - lb], eps, xm, d_slots + (l0.offset - off0), d_edges,
+                                                       st);
                 } else {
-                    stats.sample_bytes += (double)l.count * (double)(amp_bytes << bb);
+                    stats.sample_bytes += (double)draws * (double)(amp_bytes << bb);
                 }
-                stats.launches += 2;
-                stats.draws += l.count;
+                if (ctx.timer) ctx.timer->end(st, 0.0, 1);
+                stats.launches += 3;
+                stats.draws += draws;
+                stats.sampled_vectors++;
             }
-            stats.leaves++;
+            stats.leaves += g.l1 - g.l0;
             if (!dry) {
                 cudaError_t e = cudaPeekAtLastError();
                 if (e != cudaSuccess) {
@@ -381,17 +483,34 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
         }
         if (fuse) planner.materialize(ctx);   // leave the caller's buffer in logical order
         if (!dry) {
-            if (sample && off1 > off0)
+            TQ_RUN_CUDA(cudaEventRecord(ev[1], st));
+            if (comm && sample) {   // the disjoint slot arrays of all ranks, summed on the device
+                std::string err;
+                TQ_RUN_CUDA(cudaEventRecord(ev[2], st));
+                if (comm_allreduce_u64(comm, d_slots, nslots, st, err) != TUSQ_OK) {
+                    cleanup();
+                    return fail(TUSQ_ERR_NCCL, err);
+                }
+                TQ_RUN_CUDA(cudaEventRecord(ev[3], st));
+            }
+            if (sample && off1 > off0) {
                 TQ_RUN_CUDA(cudaMemcpyAsync(out_slots + off0, d_slots, (off1 - off0) * sizeof(uint64_t),
                                             cudaMemcpyDeviceToHost, st));
+                stats.d2h_bytes += (double)(off1 - off0) * 8;
+            }
             uint32_t h_edges = 0;
             TQ_RUN_CUDA(cudaMemcpyAsync(&h_edges, d_edges, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            stats.d2h_bytes += 4;
             TQ_RUN_CUDA(cudaStreamSynchronize(st));
+            float ms = 0;
+            if (cudaEventElapsedTime(&ms, ev[0], ev[1]) == cudaSuccess) stats.device_seconds = ms * 1e-3;
+            if (comm && sample && cudaEventElapsedTime(&ms, ev[2], ev[3]) == cudaSuccess) stats.reduce_seconds = ms * 1e-3;
             stats.edge_draws = h_edges;
             timer.flush();
             stats.gate_kernel_launches = timer.launches;
             stats.gate_kernel_seconds = timer.seconds;
             stats.gate_kernel_bytes = timer.bytes;
+            stats.sample_kernel_seconds = timer.sample_seconds;
         }
     } catch (const std::exception &e) {
         cleanup();

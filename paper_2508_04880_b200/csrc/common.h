@@ -83,6 +83,32 @@ struct Leaf {
     uint64_t count = 0, offset = 0;
 };
 
+// The executed part of a leaf: its triples before the readout (pos < L), and the readout flips
+// (terminal X triples at pos = L) as a bit mask.  Measurement noise is a classical flip of the
+// drawn bitstring (reading #7): leaves that differ only in terminal
+// flips share one state vector and one CDF.
+inline Leaf core_of(const Leaf &l, uint32_t L, uint64_t *tmask)
+{
+    Leaf c;
+    c.count = l.count;
+    c.offset = l.offset;
+    uint64_t m = 0;
+    for (const Triple &x : l.tr) {
+        if (x.pos < L) c.tr.push_back(x);
+        else if (x.p == 1 || x.p == 2) m ^= 1ull << x.q;   // terminal X (Y reads as X; Z never emitted)
+    }
+    if (tmask) *tmask = m;
+    return c;
+}
+
+inline bool same_core(const Leaf &a, const Leaf &b)
+{
+    if (a.tr.size() != b.tr.size()) return false;
+    for (size_t i = 0; i < a.tr.size(); ++i)
+        if (a.tr[i].pos != b.tr[i].pos || a.tr[i].q != b.tr[i].q || a.tr[i].p != b.tr[i].p) return false;
+    return true;
+}
+
 }  // namespace tq
 
 struct tusq_tree {

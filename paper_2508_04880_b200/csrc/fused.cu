@@ -891,43 +891,43 @@ GateTimer::~GateTimer()
 
 void GateTimer::begin(cudaStream_t st)
 {
+    // the pool grows as needed and is read once, at the end of the call (no host sync mid-run)
     if (!on_) return;
     if (used_ == a_.size()) {
-        if (a_.size() >= 256) flush();
-        if (used_ == a_.size()) {
-            cudaEvent_t x, y;
-            cudaEventCreate(&x);
-            cudaEventCreate(&y);
-            a_.push_back(x);
-            b_.push_back(y);
-            by_.push_back(0);
-        }
+        cudaEvent_t x, y;
+        cudaEventCreate(&x);
+        cudaEventCreate(&y);
+        a_.push_back(x);
+        b_.push_back(y);
+        by_.push_back(0);
+        cat_.push_back(0);
     }
     cudaEventRecord(a_[used_], st);
 }
 
-void GateTimer::end(cudaStream_t st, double bytes, const char *tag)
+void GateTimer::end(cudaStream_t st, double bytes, int cat)
 {
     if (!on_) return;
     cudaEventRecord(b_[used_], st);
     by_[used_] = bytes;
-    if (tags_.size() <= used_) tags_.resize(used_ + 1);
-    tags_[used_] = tag ? tag : "";
+    cat_[used_] = (uint8_t)cat;
     ++used_;
 }
 
 void GateTimer::flush()
 {
     if (!on_ || !used_) return;
-    static const bool trace = getenv("TUSQ_TRACE_LAUNCHES") != nullptr;
     cudaEventSynchronize(b_[used_ - 1]);
     for (size_t i = 0; i < used_; ++i) {
         float ms = 0;
         cudaEventElapsedTime(&ms, a_[i], b_[i]);
-        seconds += ms * 1e-3;
-        bytes += by_[i];
-        ++launches;
-        if (trace) fprintf(stderr, "[launch] %.3f ms %s\n", ms, tags_[i].c_str());
+        if (cat_[i] == 0) {
+            seconds += ms * 1e-3;
+            bytes += by_[i];
+            ++launches;
+        } else {
+            sample_seconds += ms * 1e-3;
+        }
     }
     used_ = 0;
 }
@@ -935,6 +935,8 @@ void GateTimer::flush()
 static void count(Ctx &ctx, double bytes, bool fused)
 {
     ctx.stats->launches++;
+    // kernel parameters travel with the launch: the K5 block, or a few scalars
+    ctx.stats->h2d_bytes += fused ? (double)sizeof(Params) : 64.0;
     ctx.stats->sweeps++;
     ctx.stats->hbm_bytes += bytes;
     if (fused) ctx.stats->fused_launches++;
@@ -985,10 +987,9 @@ void execute_unfused(const std::vector<Op> &ops, Ctx &ctx)
     }
 }
 
-FusedPlanner::FusedPlanner(uint32_t n, int prec, uint32_t tile_bits)
+FusedPlanner::FusedPlanner(uint32_t n, int prec)
     : n_(n), prec_(prec), tile_bits_(TB), enabled_(n >= (uint32_t)TB)
 {
-    (void)tile_bits;
 }
 
 static bool diag_of(const Op &o, double d[4]);
@@ -1001,7 +1002,7 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
     const uint64_t low = 7;   // qubits 0,1,2 are always tile qubits
     // tile qubits a group may claim beyond 0-2 (default all 9; fewer leave fillers 3, 4... in the
     // tile, i.e. longer contiguous runs per tile row, at the price of more sweeps)
-    static const int hi_cap = getenv("TUSQ_HI_CAP") ? atoi(getenv("TUSQ_HI_CAP")) : TB - 3;
+    constexpr int hi_cap = TB - 3;
     std::vector<Group> groups;
     Group g;
     uint64_t touched = 0;
@@ -1035,10 +1036,9 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
         touched = 0;
     };
     // a Toffoli core H(t) [classical run] H(t) starting at op i: the qubits it touches (0: none)
-    static const bool no_core_groups = getenv("TUSQ_NO_CORE_GROUPS") != nullptr;
     auto core_qubits = [&](size_t i) -> uint64_t {
         const Op &h = ops[i];
-        if (no_core_groups || h.kind != H) return 0;
+        if (h.kind != H) return 0;
         uint64_t m = bit(h.q0);
         double d[4];
         for (size_t j = i + 1; j < ops.size(); ++j) {
@@ -1129,6 +1129,13 @@ struct Built {
     size_t prm_used = 0;   // doubles of P.prm the records use
 };
 
+}  // namespace tq
+struct tq::PlanScratch {
+    Built B;
+    uint16_t V[tq::fk::NT][tq::fk::NR], M[1 << tq::fk::TB];   // gather-table simulation
+};
+namespace tq {
+
 // parameter doubles a record reads at prm[pi]
 static int rec_nparams(const GRec &r)
 {
@@ -1194,7 +1201,7 @@ static bool diag_of(const Op &o, double d[4])
     }
 }
 
-static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
+static void build_params(const Group &G, uint32_t n, Built &B)
 {
     Params &P = B.P;
     memset(&P, 0, sizeof(P));
@@ -1381,7 +1388,6 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
     // the ops since the last H(t) -- or since the H(t) before it, H(t) run H(t) -- are all
     // classical, the records from that H on are dropped and re-planned in the new phase, so that
     // the core folds into one table (and one C_CU record) instead of being cut in two.
-    static const bool no_backup = getenv("TUSQ_NO_BACKUP") != nullptr;
     std::vector<size_t> rec_at(G.ops.size(), SIZE_MAX), prm_at(G.ops.size(), SIZE_MAX);
     size_t phase_op0 = 0;
     auto classical_kind = [&](const Op &o) {
@@ -1390,7 +1396,7 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
     };
     for (size_t i = 0; i < G.ops.size(); ++i) {
         if (phases.empty() || needs_switch(i, regset)) {
-            if (!phases.empty() && !no_backup) {
+            if (!phases.empty()) {
                 size_t k = i;
                 while (k > phase_op0 && classical_kind(G.ops[k - 1].op)) --k;
                 const Op &oi = G.ops[i].op;
@@ -1535,7 +1541,6 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
     // ladders of a QFT, ~30 per H at 34 qubits) merge into one C_TDK record: the kernel multiplies
     // the per-thread scalar factors first and touches the amplitudes once.
     {
-        static const bool no_tdk = getenv("TUSQ_NO_TDK") != nullptr;
         std::vector<GRec> m;
         m.reserve(recs.size());
         std::vector<uint16_t> newidx(recs.size() + 1);
@@ -1543,7 +1548,7 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
             newidx[j] = (uint16_t)m.size();
             const uint16_t c0 = recs[j].code;
             size_t k = j;
-            if (!no_tdk && c0 >= C_TD1 && c0 < C_TD1 + RB)
+            if (c0 >= C_TD1 && c0 < C_TD1 + RB)
                 while (k < recs.size() && recs[k].code == c0 && k - j < 255) ++k;
             if (k - j >= 2) {
                 GRec r;
@@ -1575,7 +1580,6 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
     // Toffoli three blocks are the identity and the fourth is a plain swap.
     B.h_absorbed = 0;
     {
-        static const bool no_cu = getenv("TUSQ_NO_CU") != nullptr;
         std::vector<GRec> m;
         m.reserve(recs.size());
         std::vector<uint16_t> newidx(recs.size() + 1);
@@ -1593,7 +1597,7 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                     xs ^= 1u << (recs[k2].code - C_X);
                     ++k2;
                 }
-            if (!no_cu && k2 < recs.size() && c0 < C_H + RB && recs[k2].code == c0 && recs[j + 1].code >= C_DK &&
+            if (k2 < recs.size() && c0 < C_H + RB && recs[k2].code == c0 && recs[j + 1].code >= C_DK &&
                 recs[j + 1].code < C_DK + NR) {
                 const int p = c0 - C_H, mask = recs[j + 1].code - C_DK;
                 int jj = -1;
@@ -1655,13 +1659,7 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
                     }
                     GRec r;
                     memset(&r, 0, sizeof(r));
-                    static const bool no_ccx = getenv("TUSQ_NO_CCX") != nullptr;
-                    if (getenv("TUSQ_DEBUG_PLAN")) {
-                        fprintf(stderr, "  cu p %d j %d kinds %x unit %x t2 %d:", p, jj, kinds, unit, t2 != nullptr);
-                        for (int q = 0; q < 32; ++q) fprintf(stderr, " %.3g", blk[q] - (fabs(blk[q]) > 0.5 ? (blk[q] > 0 ? 1 : -1) : 0));
-                        fprintf(stderr, "\n");
-                    }
-                    if (!no_ccx && kinds == (2u << 6) && unit == 8u && code_ok(C_CCX + 6 * p + jj)) {
+                    if (kinds == (2u << 6) && unit == 8u && code_ok(C_CCX + 6 * p + jj)) {
                         // an error-free Toffoli: a pure register permutation (compile-time swaps,
                         // no block dispatch; absorbable into phase entry/exit offsets)
                         r.code = (uint16_t)(C_CCX + 6 * p + jj);
@@ -1692,100 +1690,6 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
         newidx[recs.size()] = (uint16_t)m.size();
         for (auto &ph : phases) { ph.g0 = newidx[ph.g0]; ph.g1 = newidx[ph.g1]; }
         recs.swap(m);
-    }
-    // Tunables (environment, for measurement): TUSQ_SPLIT_MIN (>= 2 enables phase splits after
-    // permutation runs), TUSQ_STORE_XPOSE=1 (coalescing transpose before the store).
-    static const size_t split_min = getenv("TUSQ_SPLIT_MIN") ? (size_t)atoi(getenv("TUSQ_SPLIT_MIN")) : 1000;
-    // store transpose (opt-in): superseded by paired 32-byte stores when qubit 0 ends in a register
-    // (the UMA group that ends on qubits 0-4 in registers wrote 2x the L2 sectors: 13.9 ms; with a
-    // store transpose 12.4 ms)
-    static const bool store_xpose = getenv("TUSQ_STORE_XPOSE") && getenv("TUSQ_STORE_XPOSE")[0] == '1';
-    // Split a phase right after an interior run of >= 2 register-permutation records (e.g. the
-    // two trailing CXs of every Cuccaro UMA): the run then ends its phase and is absorbed into the
-    // transpose that follows (same register set), trading ~2 swap passes for one transpose.
-    {
-        std::vector<GRec> out;
-        std::vector<Phase> nph;
-        out.reserve(recs.size() + 8);
-        for (size_t p = 0; p < phases.size(); ++p) {
-            Phase ph = phases[p];
-            if (p > 0) {
-                GRec x = recs[ph.g0 - 1];   // the transpose entering this phase
-                x.a = (uint8_t)nph.size();
-                out.push_back(x);
-            }
-            const size_t g0 = ph.g0, g1 = ph.g1;
-            ph.g0 = (uint16_t)out.size();
-            size_t j = g0;
-            while (j < g1) {
-                size_t k = j;
-                while (k < g1 && is_perm_rec(recs[k].code)) ++k;
-                const bool interior = j > g0 && k < g1;
-                // measured (launch traces, least squares): a transpose costs ~1.3 ms per 30-qubit
-                // sweep (a full shared-memory pass is >= 0.93 ms at 37 TB/s) vs ~0.5 ms per swap
-                // record, so split only for runs of >= split_min records (default: never)
-                if (k - j >= split_min && interior && nph.size() + (phases.size() - p) < (size_t)MAXPH - 2) {
-                    for (size_t q = j; q < k; ++q) out.push_back(recs[q]);
-                    ph.g1 = (uint16_t)out.size();
-                    nph.push_back(ph);
-                    GRec x;
-                    memset(&x, 0, sizeof(x));
-                    x.code = C_XPOSE;
-                    x.a = (uint8_t)nph.size();
-                    out.push_back(x);
-                    Phase cont = phases[p];   // same register set and layout
-                    cont.g0 = (uint16_t)out.size();
-                    ph = cont;
-                    j = k;
-                    continue;
-                }
-                if (k == j) { out.push_back(recs[j]); ++j; }
-                else { for (size_t q = j; q < k; ++q) out.push_back(recs[q]); j = k; }
-            }
-            ph.g1 = (uint16_t)out.size();
-            nph.push_back(ph);
-        }
-        recs.swap(out);
-        phases.swap(nph);
-    }
-    // Coalescing: global loads/stores want lanes 0-2 on tile bits 0-2 (qubits 0,1,2: 128-byte
-    // runs).  If the first (last) phase keeps one of those in a register, load (store) through an
-    // extra layout phase and one shared-memory transpose instead (measured: 32 sectors per request,
-    // 2x L2 over-fetch and LSU throttling otherwise).
-    {
-        auto low_in_regs = [&](const Phase &ph) {
-            for (int k = 0; k < RB; ++k)
-                if (ph.rl[k] < 3) return true;
-            return false;
-        };
-        auto canonical = [&]() {
-            std::vector<uint32_t> c;
-            for (uint32_t b = 3; b < (uint32_t)TB && c.size() < (size_t)RB; ++b) c.push_back(P.qs[b]);
-            return c;
-        };
-        if (will_load && low_in_regs(phases.front())) {
-            Phase c = make_phase(canonical(), 0);
-            c.g1 = 0;
-            for (auto &r : recs)
-                if (r.code == C_XPOSE) r.a++;
-            for (auto &ph : phases) { ph.g0++; ph.g1++; }
-            GRec x;
-            memset(&x, 0, sizeof(x));
-            x.code = C_XPOSE;
-            x.a = 1;
-            recs.insert(recs.begin(), x);
-            phases.insert(phases.begin(), c);
-        }
-        if (store_xpose && low_in_regs(phases.back())) {
-            GRec x;
-            memset(&x, 0, sizeof(x));
-            x.code = C_XPOSE;
-            x.a = (uint8_t)phases.size();
-            recs.push_back(x);
-            Phase c = make_phase(canonical(), (uint16_t)recs.size());
-            c.g1 = (uint16_t)recs.size();
-            phases.push_back(c);
-        }
     }
     // Absorb register permutations (in-register X, CX between register bits) at the start of a
     // phase into its entry offsets and at its end into its exit offsets: a permutation of the 32
@@ -1851,36 +1755,22 @@ static void build_params(const Group &G, uint32_t n, Built &B, bool will_load)
             cur = r.a;
         }
     }
-    static const bool dbg = getenv("TUSQ_DEBUG_PLAN") != nullptr;
-    static const bool sigs = getenv("TUSQ_DEBUG_SIGS") != nullptr;
-    if (sigs) {
-        uint64_t h = 1469598103934665603ull;
-        auto mix = [&](uint64_t v) { h ^= v; h *= 1099511628211ull; };
-        for (auto &r : recs) { mix(r.code); if (r.code >= C_TX && r.code <= C_TPH) { mix(r.a); mix(r.b); } }
-        fprintf(stderr, "[sig] %016llx %zu\n", (unsigned long long)h, recs.size());
-    }
-    if (dbg) {
-        fprintf(stderr, "[plan] ops %zu recs %zu phases %zu prm %zu tile %#llx\n", G.ops.size(), recs.size(),
+#ifdef TUSQ_DEBUG_PLAN   // build-time debug aid (TUSQ_NVCC_FLAGS=-DTUSQ_DEBUG_PLAN): print every group plan
+    {
+        fprintf(stderr, "[plan] ops %zu recs %zu phases %zu prm %zu tile %#llx\n  ops:", G.ops.size(), recs.size(),
                 phases.size(), prm.size(), (unsigned long long)tile);
-        if (getenv("TUSQ_DEBUG_PLAN")[0] == '2') {
-            for (auto &k : G.ops) fprintf(stderr, " %u(%u,%u)", k.op.kind, k.op.q0, k.op.q1);
-            fprintf(stderr, "\n  codes:");
-            for (auto &r : recs) fprintf(stderr, " %u", r.code);
-            for (auto &r : recs)
-                if (r.code >= C_DK && r.code < C_CX2) {
-                    fprintf(stderr, "\n  dk %u:", r.code - C_DK);
-                    for (int e = 0; e < (2 << __builtin_popcount(r.code - C_DK)); ++e)
-                        fprintf(stderr, " %.3f", prm[r.pi + e]);
-                }
-            fprintf(stderr, "\n  phases:");
-            for (auto &ph : phases) {
-                fprintf(stderr, " [g%u-%u regs", ph.g0, ph.g1);
-                for (int k = 0; k < RB; ++k) fprintf(stderr, " %u", P.qs[ph.rl[k]]);
-                fprintf(stderr, "]");
-            }
-            fprintf(stderr, "\n");
+        for (auto &k : G.ops) fprintf(stderr, " %u(%u,%u)", k.op.kind, k.op.q0, k.op.q1);
+        fprintf(stderr, "\n  codes:");
+        for (auto &r : recs) fprintf(stderr, " %u", r.code);
+        fprintf(stderr, "\n  phases:");
+        for (auto &ph : phases) {
+            fprintf(stderr, " [g%u-%u regs", ph.g0, ph.g1);
+            for (int k = 0; k < RB; ++k) fprintf(stderr, " %u", P.qs[ph.rl[k]]);
+            fprintf(stderr, "]");
         }
+        fprintf(stderr, "\n");
     }
+#endif
     std::copy(phases.begin(), phases.end(), P.ph);
     std::copy(recs.begin(), recs.end(), P.g);
     std::copy(prm.begin(), prm.end(), P.prm);
@@ -1916,11 +1806,9 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     if (sums_written) *sums_written = false;
     // strict grouping when it costs (almost) no extra sweeps -- e.g. ripple-carry ladders --
     // otherwise tile membership for controls/diagonals only while there is room (e.g. QFT)
-    static const char *mode_env = getenv("TUSQ_TILE_MODE");
-    static const int mode = !mode_env ? 0 : (mode_env[0] == 's' ? 1 : mode_env[0] == 'l' ? 2 : 0);
-    bool strict = mode == 1;
-    std::vector<Group> groups = make_groups(ops, strict);
-    if (mode == 0) {
+    bool strict = false;
+    std::vector<Group> groups = make_groups(ops, false);
+    {
         std::vector<Group> g2 = make_groups(ops, true);
         if (g2.size() * 100 <= groups.size() * 105) { groups.swap(g2); strict = true; }
     }
@@ -1951,7 +1839,8 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         xmask_ = 0;
         return true;
     }
-    static Built B;   // large parameter block, reused (host planner is single-threaded per call)
+    if (!scratch_) scratch_ = std::make_shared<PlanScratch>();
+    Built &B = scratch_->B;
     for (size_t gi = 0; gi < groups.size(); ++gi) {
         const Group &G = groups[gi];
         if (G.ops.empty() && !pending_init) {   // pure relabel
@@ -1959,7 +1848,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             continue;
         }
         // loads go through shared memory (always coalesced): no load-layout phase needed
-        build_params(G, n_, B, false);
+        build_params(G, n_, B);
         Params &P = B.P;
         uint64_t m_load = (pending_init ? 0 : xmask_) ^ G.xb;
         P.xm_load = m_load;
@@ -1996,13 +1885,6 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                     for (int r = 0; r < NR; ++r) P.st_odd |= (uint32_t)(P.gs[r] & 1) << r;
                 }
             }
-            static const bool no_pair = getenv("TUSQ_NO_PAIR_STORE") != nullptr;
-            if (no_pair) P.st_pair = 0;
-            if (getenv("TUSQ_DEBUG_PLAN")) {
-                fprintf(stderr, "  st_pair %u gs:", P.st_pair);
-                for (int r = 0; r < NR; ++r) fprintf(stderr, " %llx", (unsigned long long)P.gs[r]);
-                fprintf(stderr, "\n");
-            }
             // shared-memory staging of loads: copy-slot offsets, tile-local XOR mask, last transpose
             P.mloc = 0;
             for (int b = 0; b < TB; ++b)
@@ -2018,11 +1900,11 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             // ladders of an Adder group) fold into the first shared-memory read: the data movement of
             // the whole chain is simulated here and the read becomes a gather through a table
             P.gtab = 0xFFFFu;
-            static const bool no_gather = getenv("TUSQ_NO_GATHER") != nullptr;
             uint32_t kstar = 0;
             while (kstar < P.ngate && P.g[kstar].code == C_XPOSE) ++kstar;
-            if (!no_gather && !pending_init && kstar > 0 && B.prm_used + NR * NT / 4 <= (size_t)MAXP) {
-                static uint16_t V[NT][NR], M[1 << TB];
+            if (!pending_init && kstar > 0 && B.prm_used + NR * NT / 4 <= (size_t)MAXP) {
+                auto &V = scratch_->V;
+                auto &M = scratch_->M;
                 auto tt = [&](const Phase &ph, uint32_t t) {
                     uint32_t x = 0;
                     for (int j = 0; j < NTB; ++j) x |= ((t >> j) & 1u) << ph.tl[j];
@@ -2113,26 +1995,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 k_fused<double><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((double2 *)ctx.psi, P, d_sums);
             else
                 k_fused<float><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((float2 *)ctx.psi, P, d_sums);
-            static const bool sync_launch = getenv("TUSQ_SYNC_LAUNCH") != nullptr;   // measurement aid
-            if (sync_launch) cudaStreamSynchronize(ctx.st);
-            if (ctx.timer) {
-                static const bool trace = getenv("TUSQ_TRACE_LAUNCHES") != nullptr;
-                char tag[160] = "";
-                if (trace) {
-                    int cnt[9] = {0};   // H, DK, CX/CX2, D1/D2, XPOSE, X/Y, T*, other, CU
-                    for (uint32_t i = 0; i < P.ngate; ++i) {
-                        const uint16_t c = P.g[i].code;
-                        int k = c < C_U ? 0 : (c >= C_DK && c < C_CX2) ? 1 : ((c >= C_CX && c < C_CPH) || (c >= C_CX2 && c < C_CU)) ? 2
-                                : (c >= C_D1 && c < C_CX) ? 3 : c == C_XPOSE ? 4 : (c >= C_X && c < C_D1) ? 5
-                                : (c >= C_TX && c <= C_TPH) ? 6 : (c >= C_CU && c < C_CCX) ? 8 : (c >= C_CCX && c < C_TDK) ? 2 : (c >= C_TDK && c < C_N) ? 3 : 7;
-                        cnt[k]++;
-                    }
-                    snprintf(tag, sizeof(tag), "ops %zu recs %u ph %u init %d tile %#llx H%d DK%d CX%d D%d XP%d XY%d T%d O%d CU%d",
-                             G.ops.size(), P.ngate, P.nphase, pending_init ? 1 : 0, (unsigned long long)B.tile, cnt[0],
-                             cnt[1], cnt[2], cnt[3], cnt[4], cnt[5], cnt[6], cnt[7], cnt[8]);
-                }
-                ctx.timer->end(ctx.st, bytes, tag);
-            }
+            if (ctx.timer) ctx.timer->end(ctx.st, bytes);
         }
         count(ctx, bytes, true);
         pending_init = false;

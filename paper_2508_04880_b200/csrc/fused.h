@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -9,23 +10,24 @@
 
 namespace tq {
 
-// CUDA-event brackets around gate-kernel launches (TUSQ_EXEC_PROFILE).
+// CUDA-event brackets around kernel launches (TUSQ_EXEC_PROFILE): category 0 = gate kernels
+// (K1-K5, K7), 1 = sampler kernels (K6).  Read once by flush() at the end of a call.
 class GateTimer {
 public:
     explicit GateTimer(bool on) : on_(on) {}
     ~GateTimer();
     bool on() const { return on_; }
     void begin(cudaStream_t st);
-    void end(cudaStream_t st, double bytes, const char *tag = nullptr);
+    void end(cudaStream_t st, double bytes, int cat = 0);
     void flush();                 // synchronizes the recorded events and accumulates
     uint64_t launches = 0;
-    double seconds = 0.0, bytes = 0.0;
+    double seconds = 0.0, bytes = 0.0, sample_seconds = 0.0;
 
 private:
     bool on_;
     std::vector<cudaEvent_t> a_, b_;
     std::vector<double> by_;
-    std::vector<std::string> tags_;
+    std::vector<uint8_t> cat_;
     size_t used_ = 0;
 };
 
@@ -44,9 +46,13 @@ struct Ctx {
 // sweeps (physical index = logical index XOR mask).
 struct InitState { uint64_t index; double re, im; };   // reset target (K7 fused into the first sweep)
 
+struct PlanScratch;   // the K5 parameter block under construction (fused.cu), one per planner
+
+// Thread safety: a planner is used by one host thread at a time; distinct planners (and so
+// concurrent tusq_run_tree / tusq_apply_ops calls) share no mutable state.
 class FusedPlanner {
 public:
-    FusedPlanner(uint32_t n, int prec, uint32_t tile_bits);
+    FusedPlanner(uint32_t n, int prec);
     uint32_t tile_bits() const { return tile_bits_; }
     bool enabled() const { return enabled_; }
     void execute(const std::vector<Op> &ops, Ctx &ctx);
@@ -65,10 +71,17 @@ private:
     uint32_t tile_bits_;
     bool enabled_;
     uint64_t xmask_ = 0;
+    std::shared_ptr<PlanScratch> scratch_;
 };
 
 // one kernel per gate (K1-K4); consecutive Paulis on distinct qubits merge into one K4 pass
 void execute_unfused(const std::vector<Op> &ops, Ctx &ctx);
+
+// communicators (sharded.cu)
+bool comm_is_local(const tusq_comm *c);
+int comm_rank(const tusq_comm *c);
+int comm_nranks(const tusq_comm *c);
+tusq_status comm_allreduce_u64(tusq_comm *c, uint64_t *d, uint64_t n, cudaStream_t st, std::string &err);
 
 // tusq_run_tree in TUSQ_MODE_SHARDED (sharded.cu)
 tusq_status run_tree_sharded(const tusq_tree *t, const tusq_exec *ex, uint64_t *out_slots, tusq_run_stats *stats);

@@ -5,6 +5,7 @@
 // SM count, two independent pairs per thread in flight.  Bytes per launch are the
 // algorithmic bytes of SURVEY.md 8(d): 2*2^n*s for dense/X-type, 2^n*s for the
 // half-touching CX / diagonal / Z-only kernels (s = 16 B c128, 8 B c64).
+#include <atomic>
 #include <cstdio>
 
 #include "kernels.h"
@@ -43,14 +44,18 @@ __device__ __forceinline__ uint64_t insert0(uint64_t j, uint32_t q)
 
 int device_sm_count()
 {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+    // per-device cache (benign concurrent first fills: every writer stores the same value)
+    static std::atomic<int> sms[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::atomic<int> &slot = sms[dev & 63];
+    int v = slot.load(std::memory_order_relaxed);
+    if (!v) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 148;
+        slot.store(v, std::memory_order_relaxed);
     }
-    return sms;
+    return v;
 }
 
 static unsigned grid_for(uint64_t work, unsigned threads, unsigned per_thread)
@@ -321,18 +326,31 @@ double launch_init_basis(void *psi, uint32_t n, int prec, uint64_t index, double
 // Inverse-CDF draws from |amp|^2: block sums over contiguous blocks of
 // 2^block_bits amplitudes -> exclusive prefix over blocks -> per draw a binary search over
 // blocks and a warp-shuffle scan inside the chosen block.  Sums in fp64 for both precisions.
-template <typename R>
+template <typename R, int PER>
 __global__ void __launch_bounds__(TPB) k_block_sums(const typename CV<R>::T *__restrict__ psi, uint32_t block_bits,
                                                     double *__restrict__ out)
 {
+    // PER > 0: the block is PER * TPB amplitudes and every load is issued before the first use
+    // (PER independent 16-byte loads in flight per thread); PER = 0: generic strided loop
     using V = typename CV<R>::T;
     const uint64_t bs = 1ull << block_bits;
     const uint64_t base = (uint64_t)blockIdx.x * bs;
     double acc = 0.0;
-    for (uint64_t i = threadIdx.x; i < bs; i += blockDim.x) {
-        V a = psi[base + i];
-        double re = a.x, im = a.y;
-        acc += re * re + im * im;
+    if constexpr (PER > 0) {
+        V a[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) a[k] = __ldcs(psi + base + threadIdx.x + k * TPB);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const double re = a[k].x, im = a[k].y;
+            acc += re * re + im * im;
+        }
+    } else {
+        for (uint64_t i = threadIdx.x; i < bs; i += blockDim.x) {
+            V a = psi[base + i];
+            double re = a.x, im = a.y;
+            acc += re * re + im * im;
+        }
     }
     __shared__ double red[TPB / 32];
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
@@ -349,8 +367,14 @@ double launch_block_sums(const void *psi, uint32_t n, int prec, uint32_t block_b
                          cudaStream_t st)
 {
     uint64_t nb = 1ull << (n - block_bits);
-    if (prec == 64) k_block_sums<float><<<(unsigned)nb, TPB, 0, st>>>((const float2 *)psi, block_bits, d_blocks);
-    else k_block_sums<double><<<(unsigned)nb, TPB, 0, st>>>((const double2 *)psi, block_bits, d_blocks);
+    const bool fast = block_bits == 12;
+    if (prec == 64) {
+        if (fast) k_block_sums<float, 16><<<(unsigned)nb, TPB, 0, st>>>((const float2 *)psi, block_bits, d_blocks);
+        else k_block_sums<float, 0><<<(unsigned)nb, TPB, 0, st>>>((const float2 *)psi, block_bits, d_blocks);
+    } else {
+        if (fast) k_block_sums<double, 16><<<(unsigned)nb, TPB, 0, st>>>((const double2 *)psi, block_bits, d_blocks);
+        else k_block_sums<double, 0><<<(unsigned)nb, TPB, 0, st>>>((const double2 *)psi, block_bits, d_blocks);
+    }
     return (double)(1ull << n) * (prec == 64 ? 8.0 : 16.0);
 }
 
@@ -420,10 +444,16 @@ template <typename R>
 __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restrict__ psi, uint32_t block_bits,
                                                const double *__restrict__ phys, const double *__restrict__ sprefix,
                                                uint64_t nb, uint64_t n_draws, uint32_t k0, uint32_t k1,
-                                               uint64_t leaf, double edge_eps, uint64_t xm,
+                                               uint64_t leaf, const uint64_t *__restrict__ ltab, uint32_t nlt,
+                                               uint64_t omask, double edge_eps, uint64_t xm,
                                                uint64_t *__restrict__ out, uint32_t *__restrict__ edges,
                                                double tg_total, double tg_lo, double tg_hi, uint64_t ohi)
 {
+    // Leaves that share one state vector (they differ only in terminal X flips, DESIGN reading #7:
+    // measurement noise relabels the drawn bitstring) are drawn in ONE launch: ltab holds
+    // the group's nlt + 1 slot offsets (relative, ascending) then its nlt readout masks; warp w is
+    // slot w of the group, draw j = w - ltab[k] of leaf leaf + k, outcome XOR masks[k].  Without a
+    // table: draw w of `leaf`, outcome XOR omask.
     // sharded mode (tg_total > 0): the draw's point t = u * tg_total on the CDF over all shards in
     // logical order; this shard owns [tg_lo, tg_hi) and searches t - tg_lo locally, writing
     // ohi | local index (ohi = the shard's global bits)
@@ -432,7 +462,19 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned lane = threadIdx.x & 31;
     if (warp >= n_draws) return;
-    U4 w = philox10(U4{(uint32_t)warp, (uint32_t)leaf, (uint32_t)(leaf >> 32), TAG_SHOT}, k0, k1);
+    uint64_t dj = warp, dl = leaf;
+    uint64_t om = omask;
+    if (ltab) {
+        uint32_t lo = 0, hi = nlt - 1;   // last k with ltab[k] <= warp
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (ltab[mid] <= warp) lo = mid; else hi = mid - 1;
+        }
+        dj = warp - ltab[lo];
+        dl = leaf + lo;
+        om = ltab[nlt + 1 + lo];
+    }
+    U4 w = philox10(U4{(uint32_t)dj, (uint32_t)dl, (uint32_t)(dl >> 32), TAG_SHOT}, k0, k1);
     uint64_t x = (uint64_t)w.x | ((uint64_t)w.y << 32);
     const uint64_t nsb = (nb + SB - 1) / SB;
     const uint64_t mh = xm >> block_bits;
@@ -522,7 +564,7 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
             k = b * bs + kk;
             double gap = fmin(t - prev, run - t);
             edge = !found || gap < edge_eps;
-            out[warp] = k | ohi;
+            out[warp] = (k | ohi) ^ om;
             if (edge) atomicAdd(edges, 1u);
         }
     } else {
@@ -533,15 +575,16 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
                 V a = blk[i];
                 if (a.x != 0 || a.y != 0) { kk = i; break; }
             }
-            out[warp] = (b * bs + kk) | ohi;
+            out[warp] = ((b * bs + kk) | ohi) ^ om;
             atomicAdd(edges, 1u);
         }
     }
 }
 
 double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
-                    const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, double edge_eps,
-                    uint64_t xm, uint64_t *d_out, uint32_t *d_edges, cudaStream_t st)
+                    const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, const uint64_t *d_ltab,
+                    uint32_t nlt, uint64_t omask, double edge_eps, uint64_t xm, uint64_t *d_out, uint32_t *d_edges,
+                    cudaStream_t st)
 {
     if (!n_draws) return 0.0;
     uint64_t nb = 1ull << (n - block_bits);
@@ -549,18 +592,19 @@ double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, 
     uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
     if (prec == 64)
         k_draws<float><<<grid, TPB, 0, st>>>((const float2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0, k1,
-                                             leaf, edge_eps, xm, d_out, d_edges, 0.0, 0.0, 0.0, 0);
+                                             leaf, d_ltab, nlt, omask, edge_eps, xm, d_out, d_edges, 0.0, 0.0, 0.0, 0);
     else
         k_draws<double><<<grid, TPB, 0, st>>>((const double2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0,
-                                              k1, leaf, edge_eps, xm, d_out, d_edges, 0.0, 0.0, 0.0, 0);
+                                              k1, leaf, d_ltab, nlt, omask, edge_eps, xm, d_out, d_edges, 0.0, 0.0, 0.0,
+                                              0);
     return (double)n_draws * (double)(1ull << block_bits) * (prec == 64 ? 8.0 : 16.0);
 }
 
 // sharded mode: the draws of one leaf that fall into this shard's CDF window [t_lo, t_hi)
 double launch_draws_window(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
-                           const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, double edge_eps,
-                           uint64_t *d_out, uint32_t *d_edges, double t_total, double t_lo, double t_hi, uint64_t ohi,
-                           cudaStream_t st)
+                           const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, uint64_t omask,
+                           double edge_eps, uint64_t *d_out, uint32_t *d_edges, double t_total, double t_lo,
+                           double t_hi, uint64_t ohi, cudaStream_t st)
 {
     if (!n_draws) return 0.0;
     uint64_t nb = 1ull << (n - block_bits);
@@ -568,10 +612,12 @@ double launch_draws_window(const void *psi, uint32_t n, int prec, uint32_t block
     uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
     if (prec == 64)
         k_draws<float><<<grid, TPB, 0, st>>>((const float2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0, k1,
-                                             leaf, edge_eps, 0, d_out, d_edges, t_total, t_lo, t_hi, ohi);
+                                             leaf, nullptr, 0, omask, edge_eps, 0, d_out, d_edges, t_total, t_lo, t_hi,
+                                             ohi);
     else
         k_draws<double><<<grid, TPB, 0, st>>>((const double2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0,
-                                              k1, leaf, edge_eps, 0, d_out, d_edges, t_total, t_lo, t_hi, ohi);
+                                              k1, leaf, nullptr, 0, omask, edge_eps, 0, d_out, d_edges, t_total, t_lo,
+                                              t_hi, ohi);
     return (double)n_draws * (double)(1ull << block_bits) * (prec == 64 ? 8.0 : 16.0);
 }
 

@@ -14,17 +14,7 @@ double launch_pauli_string(void *psi, uint32_t n, int prec, uint64_t xmask, uint
 // K7: psi <- amp |index>
 double launch_init_basis(void *psi, uint32_t n, int prec, uint64_t index, double re, double im, cudaStream_t st);
 
-// ----- K5: fused tile kernel (see fused.cu) ------------------------------------------
-struct FusedPlan;
-double launch_fused(void *psi, uint32_t n, int prec, const FusedPlan &plan, cudaStream_t st,
-                    double *d_tile_sums);
-
 // ----- K6: sampler ---------------------------------------------------------------------
-struct SamplerWork {
-    double *d_blocks = nullptr;    // per-block |amp|^2 sums, then exclusive prefix (nb + 1)
-    uint64_t cap_blocks = 0;
-    uint32_t *d_edges = nullptr;   // edge-draw counter
-};
 // block sums of |amp|^2 over contiguous blocks of 2^block_bits amplitudes
 double launch_block_sums(const void *psi, uint32_t n, int prec, uint32_t block_bits, double *d_blocks,
                          cudaStream_t st);
@@ -32,10 +22,18 @@ double launch_block_sums(const void *psi, uint32_t n, int prec, uint32_t block_b
 // logical ^ mh), then their exclusive prefix: d_prefix[0..nsb] (nsb = ceil(nb/1024)); needs
 // 2*nsb + 2 doubles of d_prefix
 void launch_scan_blocks(const double *d_phys, double *d_prefix, uint64_t nb, uint64_t mh, cudaStream_t st);
-// draws j = 0..n_draws-1 of leaf `leaf` into d_out[j]; logical index i lives at physical i ^ xm
+// draws of one leaf (d_ltab = NULL: draw j -> d_out[j], outcome XOR omask) or of a group of nlt
+// consecutive leaves sharing this state (d_ltab: nlt + 1 relative slot offsets, then nlt readout
+// masks; leaf ids leaf .. leaf + nlt - 1); logical index i lives at physical i ^ xm
 double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
-                    const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, double edge_eps,
-                    uint64_t xm, uint64_t *d_out, uint32_t *d_edges, cudaStream_t st);
+                    const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, const uint64_t *d_ltab,
+                    uint32_t nlt, uint64_t omask, double edge_eps, uint64_t xm, uint64_t *d_out, uint32_t *d_edges,
+                    cudaStream_t st);
+// sharded mode: the draws of one leaf that fall into this shard's CDF window [t_lo, t_hi)
+double launch_draws_window(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
+                           const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, uint64_t omask,
+                           double edge_eps, uint64_t *d_out, uint32_t *d_edges, double t_total, double t_lo,
+                           double t_hi, uint64_t ohi, cudaStream_t st);
 
 int device_sm_count();
 

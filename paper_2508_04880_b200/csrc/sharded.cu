@@ -24,6 +24,7 @@
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include <nccl.h>
@@ -48,21 +49,21 @@ struct Api {
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 // libnccl.so.2 is resolved at first use (the one torch already loaded, if any): the library itself
-// loads and runs replica mode on machines without NCCL.
+// loads and runs replica mode on machines without NCCL.  Thread-safe (std::call_once).
 static Api &api()
 {
     static Api a;
-    static bool tried = false;
-    if (tried) return a;
-    tried = true;
-    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return a;
-#define TQ_SYM(f) a.f = reinterpret_cast<decltype(a.f)>(dlsym(h, "nccl" #f)); if (!a.f) return a;
-    TQ_SYM(GetUniqueId) TQ_SYM(CommInitRank) TQ_SYM(CommDestroy) TQ_SYM(GroupStart) TQ_SYM(GroupEnd)
-    TQ_SYM(Send) TQ_SYM(Recv) TQ_SYM(AllReduce) TQ_SYM(GetErrorString)
+    static std::once_flag once;
+    std::call_once(once, []() {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+#define TQ_SYM(f) a.f = reinterpret_cast<decltype(a.f)>(dlsym(h, "nccl" #f)); if (!a.f) return;
+        TQ_SYM(GetUniqueId) TQ_SYM(CommInitRank) TQ_SYM(CommDestroy) TQ_SYM(GroupStart) TQ_SYM(GroupEnd)
+        TQ_SYM(Send) TQ_SYM(Recv) TQ_SYM(AllReduce) TQ_SYM(GetErrorString)
 #undef TQ_SYM
-    a.ok = true;
+        a.ok = true;
+    });
     return a;
 }
 }  // namespace nccl
@@ -77,6 +78,20 @@ struct tusq_comm {
 };
 
 namespace tq {
+
+bool comm_is_local(const tusq_comm *c) { return c->local; }
+int comm_rank(const tusq_comm *c) { return c->rank; }
+int comm_nranks(const tusq_comm *c) { return c->nranks; }
+
+// replica mode: sum the ranks' (disjoint) u64 slot arrays in place on the device
+tusq_status comm_allreduce_u64(tusq_comm *c, uint64_t *d, uint64_t n, cudaStream_t st, std::string &err)
+{
+    auto &a = nccl::api();
+    if (!a.ok) { err = "libnccl.so.2 not available"; return TUSQ_ERR_NCCL; }
+    ncclResult_t r = a.AllReduce(d, d, n, ncclUint64, ncclSum, c->nc, st);
+    if (r != ncclSuccess) { err = std::string("ncclAllReduce: ") + a.GetErrorString(r); return TUSQ_ERR_NCCL; }
+    return TUSQ_OK;
+}
 
 // ---------------------------------------------------------------- device helpers
 template <typename V>
@@ -395,11 +410,6 @@ struct ShardRun {
 
 }  // namespace
 
-// K6 over shards: totals, owner search, local draws (see launch_draws_window in kernels.cu)
-double launch_draws_window(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
-                           const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, double edge_eps,
-                           uint64_t *d_out, uint32_t *d_edges, double t_total, double t_lo, double t_hi, uint64_t ohi,
-                           cudaStream_t st);
 
 tusq_status run_tree_sharded(const tusq_tree *t, const tusq_exec *ex, uint64_t *out_slots, tusq_run_stats *stats_out)
 {
@@ -454,7 +464,7 @@ tusq_status run_tree_sharded(const tusq_tree *t, const tusq_exec *ex, uint64_t *
     S.shard_of.resize(R); S.v_of.resize(R);
     S.ph.assign(R, 1.0);
     S.ops.resize(R);
-    for (uint64_t s = 0; s < R; ++s) S.planners.emplace_back(S.nl, S.prec, ex->fuse_qubits);
+    for (uint64_t s = 0; s < R; ++s) S.planners.emplace_back(S.nl, S.prec);
     S.fuse = !(ex->flags & TUSQ_EXEC_NO_FUSE) && S.planners[0].enabled();
     const uint32_t bb = S.nl < 12 ? S.nl : 12;
     const uint64_t nb = 1ull << (S.nl - bb);
@@ -498,9 +508,13 @@ tusq_status run_tree_sharded(const tusq_tree *t, const tusq_exec *ex, uint64_t *
     std::vector<Op> seq;
     uint64_t since_anchor = 0;
     try {
+        const uint32_t L = (uint32_t)t->gates.size();
+        Leaf prev_core;
         for (uint64_t li = lb; li < le; ++li) {
-            const Leaf &l = t->leaves[li];
-            const Leaf *prev = li > lb ? &t->leaves[li - 1] : nullptr;
+            // executed part of the leaf; terminal X flips relabel its draws (reading #7)
+            uint64_t omask = 0;
+            const Leaf l = core_of(t->leaves[li], L, &omask);
+            const Leaf *prev = li > lb ? &prev_core : nullptr;
             seq.clear();
             uint64_t idx = 0;
             double re = 1.0, im = 0.0;
@@ -567,15 +581,17 @@ tusq_status run_tree_sharded(const tusq_tree *t, const tusq_exec *ex, uint64_t *
                         double *bl = d_blocks + i * blk_stride;
                         if (!dry)
                             stats.sample_bytes += launch_draws_window(S.buf[s], S.nl, S.prec, bb, bl, bl + nb, l.count,
-                                                                      t->seed, li, eps, d_slots + (l.offset - off0), d_edges,
-                                                                      T, lo, hi, v << S.nl, S.st);
+                                                                      t->seed, li, omask, eps, d_slots + (l.offset - off0),
+                                                                      d_edges, T, lo, hi, v << S.nl, S.st);
                         stats.launches++;
                     }
                     lo += tot[s];
                 }
                 stats.draws += l.count;
+                stats.sampled_vectors++;
             }
             stats.leaves++;
+            prev_core = l;
             if (!dry) {
                 cudaError_t e = cudaPeekAtLastError();
                 if (e != cudaSuccess) {

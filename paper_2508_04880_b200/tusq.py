@@ -52,7 +52,10 @@ class RunStats(C.Structure):
                 ("edge_draws", C.c_uint64), ("hbm_bytes", C.c_double), ("sample_bytes", C.c_double),
                 ("host_seconds", C.c_double), ("gate_kernel_launches", C.c_uint64),
                 ("gate_kernel_seconds", C.c_double), ("gate_kernel_bytes", C.c_double),
-                ("fused_launches", C.c_uint64), ("exchanges", C.c_uint64)]
+                ("fused_launches", C.c_uint64), ("exchanges", C.c_uint64),
+                ("sample_kernel_seconds", C.c_double), ("device_seconds", C.c_double),
+                ("reduce_seconds", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double),
+                ("sampled_vectors", C.c_uint64)]
 
     def to_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -182,15 +185,21 @@ def build_error_tree(n: int, ops, p1: float, p2: float, p_meas: float, shots: in
 def run_tree(tree: Tree, precision: int = 128, d_state=None, state_bytes: int = 0, stream=None,
              leaf_begin: int = 0, leaf_end: int = 0, flags: int = 0, reanchor_budget: int = 0,
              fuse_qubits: int = 0, edge_eps: float = 0.0, device: int = -1, out_slots: Optional[np.ndarray] = None,
-             comm: Optional["Comm"] = None):
+             comm: Optional["Comm"] = None, mode: Optional[int] = None):
     """Returns (slots u64[S1], stats dict).  d_state: device pointer (int) or tensor; None = library-allocated.
-    comm: a Comm -> TUSQ_MODE_SHARDED (d_state then holds this process's shards)."""
+    comm: a Comm -> TUSQ_MODE_SHARDED by default (d_state then holds this process's shards); with
+    mode=MODE_REPLICA an NCCL Comm of the replica ranks sums the slot arrays inside the library."""
     info = tree.info()
     if out_slots is None:
         out_slots = np.zeros(info["S1"], dtype=np.uint64)
+    if not (isinstance(out_slots, np.ndarray) and out_slots.dtype == np.uint64 and out_slots.flags.c_contiguous
+            and out_slots.ndim == 1 and out_slots.size >= info["S1"]):
+        raise ValueError(f"out_slots must be a C-contiguous 1-d uint64 array of at least S1 = {info['S1']} entries")
     if d_state is not None and not state_bytes and hasattr(d_state, "numel"):
         state_bytes = d_state.numel() * d_state.element_size()
-    ex = Exec(precision, MODE_SHARDED if comm is not None else MODE_REPLICA, device, flags, _ptr(d_state),
+    if mode is None:
+        mode = MODE_SHARDED if comm is not None else MODE_REPLICA
+    ex = Exec(precision, mode, device, flags, _ptr(d_state),
               state_bytes, _ptr(stream), leaf_begin, leaf_end, reanchor_budget, fuse_qubits, 0, edge_eps,
               comm.h if comm is not None else None)
     stats = RunStats()

@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, out_dir):
+def _worker(rank, world, port, name, out_dir, real=False):
     import torch.distributed as dist
 
     import paper_2508_04880_b200 as T
@@ -37,9 +37,13 @@ def _worker(rank, world, port, name, out_dir):
 
     def run_range(b, e):
         out = np.zeros(cfg.shots, dtype=np.uint64)
+        if real:   # the library's own tusq_run_tree on cuda:0 (both ranks share the device)
+            if e > b:
+                T.run_tree(tree, 128, leaf_begin=b, leaf_end=e, out_slots=out)
+            return out
         for l in range(b, e):
             _, cnt, off = ot.leaf(l)
-            k, _ = ot.sample_leaf(ot.replay_leaf(l), l)
+            k, _ = ot.sample_leaf(ot.replay_leaf_core(l), l)
             out[off:off + cnt] = k
         return out
 
@@ -47,6 +51,28 @@ def _worker(rank, world, port, name, out_dir):
     np.save(os.path.join(out_dir, f"slots{rank}.npy"), slots)
     np.save(os.path.join(out_dir, f"range{rank}.npy"), np.array([lb, le]))
     dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C2a", "C3"])
+def test_gloo_world2_real_run_tree(tmp_path, oracle, name):
+    # both ranks run the real tusq_run_tree on cuda:0 over their tusq_tree_partition ranges; the gloo
+    # SUM of the disjoint slot arrays equals the single-rank library run and the oracle (non-edge)
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, name, str(tmp_path), True), nprocs=2, join=True)
+    s0, s1 = np.load(tmp_path / "slots0.npy"), np.load(tmp_path / "slots1.npy")
+    r0, r1 = np.load(tmp_path / "range0.npy"), np.load(tmp_path / "range1.npy")
+    assert r0[0] == 0 and r0[1] == r1[0] and r1[1] > r1[0]
+    assert np.array_equal(s0, s1)
+    import paper_2508_04880_b200 as T
+    cfg = W.config(name)
+    nz = cfg.noise
+    tree = T.build_error_tree(cfg.n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
+    single, _ = T.run_tree(tree, 128)
+    assert np.array_equal(s0, single)
+    ref, edge = oracle.Tree.from_config(cfg).run()
+    assert int(edge.sum()) <= max(3, cfg.shots // 1000)
+    assert ((s0 != ref) & ~edge).sum() == 0
 
 
 @pytest.mark.parametrize("name", ["C1", "C2a"])

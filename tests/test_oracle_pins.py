@@ -427,3 +427,36 @@ def test_sampling_examples(oracle):
     out, _ = oracle.sample_state(st, 2, 2, 0, 20000)
     assert set(np.unique(out)) <= {1, 3}
     assert abs((out == 3).mean() - 0.64) < 0.02
+
+
+# ------------------------------------------------------------------ readout relabel (reading #7)
+def test_terminal_flips_are_readout_relabels(oracle):
+    # measurement noise = an X right before readout.  The oracle samples a leaf from
+    # its core state (triples before the readout) and XORs the drawn bitstrings with the leaf's
+    # terminal X mask.  Pin: |core|^2 permuted by the mask equals |full replay|^2 EXACTLY (X is a
+    # pure permutation), and every slot of or_run is the core draw XOR the mask.
+    cfg = W.config("C2a")
+    nz = cfg.noise
+    n, ops = W.ghz(6)
+    t = oracle.Tree(n, ops, nz.p1, nz.p2, 0.05, 4096, 7)
+    idx = np.arange(1 << n)
+    seen = 0
+    for l in range(t.n_leaves):
+        tr, cnt, off = t.leaf(l)
+        mask = t.terminal_mask(l)
+        expect = 0
+        for (pos, q, p) in tr:
+            if pos == len(ops):
+                assert p == 1          # terminal triples are X flips only (Z dropped)
+                expect ^= 1 << q
+        assert mask == expect
+        seen += mask != 0
+        full = np.abs(t.replay_leaf(l)) ** 2
+        core = np.abs(t.replay_leaf_core(l)) ** 2
+        assert np.array_equal(full, core[idx ^ mask])
+    assert seen > 0
+    slots, edge = t.run()
+    for l in range(t.n_leaves):
+        _, cnt, off = t.leaf(l)
+        k, e = oracle.sample_state(t.replay_leaf_core(l), n, 7, l, cnt)
+        assert np.array_equal(slots[off:off + cnt], k ^ np.uint64(t.terminal_mask(l)))
