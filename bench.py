@@ -1,12 +1,15 @@
 #!/usr/bin/env python
 """TUSQ hot-path benchmark (BASELINE.json metric: noisy-sim wall s per circuit, 30q Adder; gate HBM GB/s).
 
-One step = one pass of the whole hot path over one batch: the ECM + tree (a1-a6, host, the full
-circuit) and the DFS traversal of the next B leaves of this rank's DFS range with uncompute /
-re-anchor, fused gate sweeps and leaf sampling (a7-a10, device).  `value` is the projected wall
-seconds per circuit: ECM seconds + (this rank's total algorithmic bytes from the exact host plan)
-/ (bytes per second measured over the timed steps), max over ranks.  `--full` runs every leaf of
-every rank's range inside the timed region instead (no projection).
+The measured quantity is ONE WHOLE CIRCUIT (C4 by default: 30-qubit noisy Adder, 8192 shots):
+the ECM + tree (a1-a6, host) and then the DFS traversal of EVERY leaf (a7-a10, device) -- uncompute /
+re-anchor, fused gate sweeps, leaf sampling -- with, for N > 1, the slot reduction over the ranks.
+A "step" is one contiguous, cost-balanced batch of this rank's DFS range: --steps K batches cover
+the whole range (each continues the DFS state of the previous one), so
+    value = ecm_s + (device seconds of the K timed steps + the reduction), max over ranks
+is the measured wall time of one circuit -- nothing is projected.  Warm-up runs W short separate
+batches first.  After the timed region an untimed PROFILE pass (per-launch CUDA events) over a few
+short batches gives the K5 per-launch time behind `roofline` and the stage shares.
 
 Launch: python bench.py --gpus N --steps K --warmup W   (N > 1 under torch.distributed.run)
         python bench.py --impl reference ...              (the CPU oracle on host cores)
@@ -33,7 +36,7 @@ def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
 
@@ -58,7 +61,7 @@ class Clocks:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self.stop.wait(0.2)
+            self.stop.wait(0.5)
 
     def __enter__(self):
         self.th.start()
@@ -80,9 +83,23 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
+def workload_desc(cfg) -> str:
+    nz = cfg.noise
+    kind = "Cuccaro adder" if cfg.name in ("C1", "C3", "C4") else ("GHZ" if cfg.name == "C2a" else "QFT")
+    return (f"{cfg.name}: {cfg.n}q {kind} (L={len(cfg.ops)}), depolarizing p1={nz.p1} p2={nz.p2}"
+            + (f" p_meas={nz.p_meas}" if nz.p_meas else "") + f", {cfg.shots} shots, seed {cfg.seed}, alpha 1/100, beta 100")
+
+
+def config_dict(cfg, prec, world):
+    """The config both arms report (identical keys and values for the same workload)."""
+    return {"workload": workload_desc(cfg), "precision": f"c{prec}", "shots": cfg.shots,
+            "l2": f"state {(16 if prec == 128 else 8) * 2 ** cfg.n / 2 ** 30:.0f} GiB >> 126 MB L2 (no flush needed)",
+            "parallelism": f"replica x{world}, contiguous cost-balanced DFS leaf ranges"}
+
+
 def cpu_oracle_rate(cfg, max_seconds: float = 20.0):
-    """Time the oracle (as it stands) applying gates of leaf 0 at the config's size on the host cores.
-    Returns (seconds per gate application, cores, sample description)."""
+    """Time the oracle (as it stands) applying gates of the circuit at the config's size on the host
+    cores.  Returns (seconds per gate application, cores, sample description)."""
     import numpy as np
     from oracle import oracle as O
     n = cfg.n
@@ -112,23 +129,18 @@ def cpu_oracle_rate(cfg, max_seconds: float = 20.0):
     return dt, cores, desc
 
 
-def workload_desc(cfg) -> str:
-    nz = cfg.noise
-    kind = "Cuccaro adder" if cfg.name in ("C1", "C3", "C4") else ("GHZ" if cfg.name == "C2a" else "QFT")
-    return (f"{cfg.name}: {cfg.n}q {kind} (L={len(cfg.ops)}), depolarizing p1={nz.p1} p2={nz.p2}"
-            + (f" p_meas={nz.p_meas}" if nz.p_meas else "") + f", {cfg.shots} shots, seed {cfg.seed}, alpha 1/100, beta 100")
-
-
-def ncu_traffic(prec, no_fuse):
-    """DRAM bytes per k_fused launch from the committed ncu --set full capture of this bench (c128)."""
-    path = os.path.join(ROOT, "profiles", "r1_ncu_k_fused_in_bench.json")
-    if no_fuse or prec != 128 or not os.path.exists(path):
-        return None
-    try:
-        caps = json.load(open(path))["full_capture"]
-        return caps[0].get("dram_traffic_bytes")
-    except (OSError, ValueError, KeyError, IndexError):
-        return None
+def ncu_traffic(prec):
+    """DRAM bytes per k_fused launch from the committed in-bench ncu --set full capture (c128)."""
+    for name in ("r2_ncu_k_fused_in_bench.json", "r1_ncu_k_fused_in_bench.json"):
+        path = os.path.join(ROOT, "profiles", name)
+        if prec != 128 or not os.path.exists(path):
+            continue
+        try:
+            caps = json.load(open(path))["full_capture"]
+            return caps[0].get("dram_traffic_bytes"), f"profiles/{name}"
+        except (OSError, ValueError, KeyError, IndexError):
+            continue
+    return None, None
 
 
 def run_reference(args, rank, world):
@@ -145,16 +157,17 @@ def run_reference(args, rank, world):
     per, cores, desc = None, None, None
     times = []
     for s in range(args.warmup + args.steps):
-        per, cores, desc = cpu_oracle_rate(cfg, max_seconds=args.cpu_seconds / 2)
+        per, cores, desc = cpu_oracle_rate(cfg, max_seconds=args.cpu_seconds / 4)
         if s >= args.warmup:
             times.append(per)
     per = sorted(times)[len(times) // 2]
     value = t_ecm + per * naive
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg), "extrapolated": True,
-                       "projection": "oracle ECM s + (oracle s per gate application) x naive gate applications"},
+            "scaling": "strong", "vs_baseline": None, "dtype": f"c{args.precision}", "data": "synthetic",
+            "config": config_dict(cfg, args.precision, world),
+            "extrapolated": True,
+            "projection": "oracle ECM s + (oracle s per gate application) x naive gate applications",
             "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -163,26 +176,30 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="tusq", choices=["tusq", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--precision", type=int, default=128, choices=[128, 64])
-    ap.add_argument("--leaves-per-step", type=int, default=0)
-    ap.add_argument("--full", action="store_true")
     ap.add_argument("--no-fuse", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-leaves", type=int, default=48,
+                    help="leaves per batch of the untimed per-launch profile pass (3 batches)")
     ap.add_argument("--mode", default="replica", choices=["replica", "sharded"],
                     help="sharded: amplitudes split over the N ranks by global qubits (e.g. --config C5 on 8 GPUs)")
     ap.add_argument("--shards", type=int, default=0,
                     help="sharded mode on ONE GPU: this many shards driven by one process (local communicator)")
+    ap.add_argument("--leaves", type=int, default=0,
+                    help="sharded mode only: time the first this-many DFS leaves (C5 at full size is ~16 GPU-hours)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.mode == "sharded":
+        return run_sharded(args, rank, world, local)
 
     import numpy as np
     import torch
@@ -191,138 +208,198 @@ def main():
     import paper_2508_04880_b200 as T
 
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2508_04880_b200 import dist as D
+        comm, _ = D.make_comm(local)
     cfg = W.config(args.config)
     nz = cfg.noise
     n = cfg.n
     prec = args.precision
-
-    # ---- ECM + tree (host): timed on the host clock (it is host work)
-    t0 = time.perf_counter()
-    tree = T.build_error_tree(n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
-    t_ecm = time.perf_counter() - t0
-    info = tree.info()
-    flags = T.EXEC_PROFILE | (T.EXEC_NO_FUSE if args.no_fuse else 0)
+    K = max(1, args.steps)
+    flags = T.EXEC_NO_FUSE if args.no_fuse else 0
     dt = torch.complex128 if prec == 128 else torch.complex64
-    comm = None
-    nshards = 0
-    if args.mode == "sharded":
-        # every rank runs every leaf on its 2^(n-g) shard; the host plan is the same on all ranks
-        if world > 1:
-            from paper_2508_04880_b200 import dist as D
-            comm, _ = D.make_sharded_comm(local)
-            nshards = world
-            state = torch.empty(1 << (n - (world.bit_length() - 1)), dtype=dt, device="cuda")
-        else:
-            # one GPU: all shards in this process (the local communicator; exchanges are device swaps)
-            nshards = args.shards or 2
-            comm = T.Comm.local(nshards)
-            state = torch.empty(1 << n, dtype=dt, device="cuda")
-        lb, le = 0, info["n_leaves"]
-        _, plan = T.run_tree(tree, prec, flags=flags | T.EXEC_PLAN_ONLY, comm=T.Comm.local(nshards))
-    else:
-        bounds = tree.partition(world, prec)
-        lb, le = int(bounds[rank]), int(bounds[rank + 1])
-        _, plan = T.run_tree(tree, prec, leaf_begin=lb, leaf_end=le, flags=flags | T.EXEC_PLAN_ONLY)
-        state = torch.empty(1 << n, dtype=dt, device="cuda")
-    plan_bytes = plan["hbm_bytes"] + plan["sample_bytes"]
+    state = torch.empty(1 << n, dtype=dt, device="cuda")
     stream = torch.cuda.current_stream()
-    nleaf = max(le - lb, 1)
-    B = args.leaves_per_step or max(1, min(nleaf, (16 if comm is not None else 64) if n >= 28 else 256))
     slots = np.zeros(cfg.shots, dtype=np.uint64)
 
-    # batches spread evenly over the rank's DFS range (the cost of a transition depends on where
-    # in the tree it is: early DFS leaves diverge late in the circuit); each batch starts with a
-    # re-anchor.  Warm-up batches come from the same spread, interleaved.
-    nb_total = args.warmup + (1 if args.full else args.steps)
-    stride = max(1, nleaf // max(nb_total, 1))
-
-    def step(s, full=False):
-        b = lb if full else lb + (s * stride) % nleaf
-        e = le if full else min(b + B, le)
-        _, st = T.run_tree(tree, prec, d_state=state, stream=stream, leaf_begin=b, leaf_end=e, flags=flags,
-                           out_slots=slots, comm=comm)
-        return st
-
-    order = list(range(nb_total))
-    warm, timed = order[1::2][:args.warmup], [s for s in order if s not in order[1::2][:args.warmup]]
-    for s in warm:
-        step(s)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stats = []
+    # ---- warm-up: W short separate batches (untimed), ECM included
+    tree = T.build_error_tree(n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
+    nl = tree.n_leaves
+    for w in range(args.warmup):
+        b = (w * 997) % max(nl - 8, 1)
+        T.run_tree(tree, prec, d_state=state, stream=stream, leaf_begin=b, leaf_end=min(b + 8, nl), flags=flags,
+                   out_slots=np.zeros(cfg.shots, dtype=np.uint64))
+    del tree
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+
+    # ---- timed: ECM (host) + K contiguous batches of this rank's range + the reduction
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    stats = []
     with Clocks(local) as clk:
         w0 = time.perf_counter()
-        ev0.record(stream)
-        for s in ([0] if args.full else timed[:args.steps]):
-            stats.append(step(s, args.full))
-        ev1.record(stream)
+        tree = T.build_error_tree(n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
+        t_ecm = time.perf_counter() - w0
+        bounds = tree.partition(world * K, prec)
+        batches = [(int(bounds[rank * K + s]), int(bounds[rank * K + s + 1])) for s in range(K)]
+        ev[0].record(stream)
+        for s, (b, e) in enumerate(batches):
+            _, st = T.run_tree(tree, prec, d_state=state, stream=stream, leaf_begin=b, leaf_end=e,
+                               flags=flags | (T.EXEC_CONTINUE if s else 0), out_slots=slots)
+            stats.append(st)
+        ev[1].record(stream)
+        if comm is not None:
+            ev[2].record(stream)
+            T.reduce_slots(comm, slots, stream)
+            ev[3].record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
-    if world > 1:
-        dist.barrier()
-    t_dev = ev0.elapsed_time(ev1) / 1e3
+    t_dev = ev[0].elapsed_time(ev[1]) / 1e3
+    t_red = ev[2].elapsed_time(ev[3]) / 1e3 if comm is not None else 0.0
     tot = {k: sum(st[k] for st in stats) for k in stats[0]}
-    done_bytes = tot["hbm_bytes"] + tot["sample_bytes"]
-    rate = done_bytes / t_dev
-    proj = t_dev if args.full else plan_bytes / rate
-    proj_wall = wall if args.full else plan_bytes / (done_bytes / wall)
-    # max over ranks
-    vals = torch.tensor([proj, proj_wall, t_dev], dtype=torch.float64, device="cuda")
+    vals = torch.tensor([t_ecm + t_dev + t_red, wall, t_dev, t_red], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    proj, proj_wall, t_dev_max = [float(x) for x in vals.cpu()]
-    value = t_ecm + proj
+    value, wall_max, t_dev_max, t_red_max = [float(x) for x in vals.cpu()]
+    info = tree.info()
+
+    # ---- untimed profile pass: per-launch CUDA events over 3 short batches spread over the range
+    lb, le = batches[0][0], batches[-1][1]
+    prof = []
+    for frac in (0.1, 0.5, 0.85):
+        b = lb + int((le - lb) * frac)
+        e = min(le, b + args.profile_leaves)
+        if e > b:
+            _, st = T.run_tree(tree, prec, d_state=state, stream=stream, leaf_begin=b, leaf_end=e,
+                               flags=flags | T.EXEC_PROFILE, out_slots=np.zeros(cfg.shots, dtype=np.uint64))
+            prof.append(st)
+    ptot = {k: sum(st[k] for st in prof) for k in prof[0]} if prof else None
     hbm_peak, peak_src = peaks()
-    gk_s, gk_b, gk_n = tot["gate_kernel_seconds"], tot["gate_kernel_bytes"], tot["gate_kernel_launches"]
-    achieved = gk_b / gk_s / 1e9 if gk_s > 0 else None
+    achieved = share_gate = share_sample = None
+    if ptot and ptot["gate_kernel_seconds"] > 0:
+        achieved = ptot["gate_kernel_bytes"] / ptot["gate_kernel_seconds"] / 1e9
+        share_gate = ptot["gate_kernel_seconds"] / ptot["device_seconds"]
+        share_sample = ptot["sample_kernel_seconds"] / ptot["device_seconds"]
+    # the same kernel's rate inside the timed steps: its bytes / (its profile share x step time)
+    in_step = (tot["hbm_bytes"] / (share_gate * t_dev) / 1e9) if share_gate else None
+    traffic, traffic_src = ncu_traffic(prec)
+    n_launch = ptot["gate_kernel_launches"] if ptot else 0
     line = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
-        "steps": 1 if args.full else args.steps, "warmup": args.warmup,
-        "ms_per_step": t_dev_max * 1e3 / (1 if args.full else args.steps),
-        "higher_is_better": False, "scaling": "strong" if args.full else "weak", "vs_baseline": None,
-        "dtype": "c128" if prec == 128 else "c64", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg),
-                   "leaves": info["n_leaves"], "leaves_per_step": B, "rank_leaves": [lb, le],
-                   "extrapolated": not args.full,
-                   "projection": "ECM s + rank plan bytes / measured bytes-per-s over the timed steps (max over ranks)",
-                   "ecm_s": t_ecm, "gpu_projected_s": proj, "plan_sweeps": plan["sweeps"],
-                   "plan_gate_apps": plan["gate_apps"], "plan_hbm_GB": plan_bytes / 1e9,
-                   "dftt_ops": info["dftt_ops"], "naive_ops": info["naive_ops"],
-                   "l2": f"state {state.numel() * state.element_size() / 2**30:.0f} GiB >> 126 MB L2 (no flush needed)",
-                   "fused": not args.no_fuse,
-                   "parallelism": (f"sharded x{nshards} over {world} GPU(s): amplitudes split by "
-                                   f"{nshards.bit_length() - 1} global qubits, half-shard exchanges "
-                                   + ("(NCCL)" if world > 1 else "(local communicator, device swaps)")
-                                   if comm is not None
-                                   else f"replica x{world}, contiguous DFS leaf ranges")},
+        "steps": K, "warmup": args.warmup, "ms_per_step": t_dev_max * 1e3 / K,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": f"c{prec}", "data": "synthetic",
+        "config": config_dict(cfg, prec, world),
+        "extrapolated": False,
+        "measured": "ECM + every DFS leaf of every rank (K contiguous batches) + slot reduction, max over ranks",
+        "stages": {"ecm_s": t_ecm, "device_s": t_dev_max, "reduce_s": t_red_max,
+                   "traversal_s": share_gate * t_dev_max if share_gate else None,
+                   "sampling_s": share_sample * t_dev_max if share_sample else None,
+                   "note": "traversal/sampling = device_s x the gate/sampler kernel shares of the profile pass"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": ncu_traffic(prec, args.no_fuse),
-                     "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one k_fused launch of this "
-                                       "bench under ncu --set full (profiles/r1_ncu_k_fused_in_bench.json)",
+                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
+                     "traffic_source": (f"dram__bytes_read.sum + dram__bytes_write.sum of one k_fused launch of this "
+                                        f"bench under ncu --set full ({traffic_src})") if traffic_src else None,
                      "kernel": "k_fused (K5)" if not args.no_fuse else "K1-K4",
-                     "launches_timed": gk_n, "bytes_per_launch": gk_b / max(gk_n, 1),
-                     "avg_launch_ms": gk_s / max(gk_n, 1) * 1e3, "peak_source": peak_src,
-                     "step_share": gk_s / t_dev if t_dev > 0 else None},
-        "e2e": {"value": t_ecm + proj_wall, "unit": "s", "h2d_bytes_per_step": 24 * len(cfg.ops),
-                "d2h_bytes_per_step": int(8 * sum(st["draws"] for st in stats) / len(stats)),
-                "note": "public API (build_error_tree + run_tree, host out_slots) on the host clock"},
+                     "per_unit": "one fused sweep = 2 x 2^n x 16 B (2^n x 16 B when it starts from a reset)",
+                     "launches_profiled": n_launch,
+                     "bytes_per_launch": ptot["gate_kernel_bytes"] / max(n_launch, 1) if ptot else None,
+                     "avg_launch_ms": ptot["gate_kernel_seconds"] / max(n_launch, 1) * 1e3 if ptot else None,
+                     "achieved_in_timed_steps": in_step, "frac_in_timed_steps": in_step / hbm_peak if in_step else None,
+                     "step_share": share_gate, "peak_source": peak_src},
+        "e2e": {"value": wall_max, "unit": "s",
+                "h2d_bytes_per_step": int(tot["h2d_bytes"] / K), "d2h_bytes_per_step": int(tot["d2h_bytes"] / K),
+                "note": "host clock around build_error_tree + every run_tree call (host op list in, host slots out) "
+                        "+ the slot reduction; h2d = kernel parameter blocks + draw tables, d2h = slots + counters"},
         "gpu_launches": int(tot["launches"]),
         "clocks": clk.summary(),
-        "stats": {k: tot[k] for k in ("leaves", "resets", "gate_apps", "sweeps", "draws", "edge_draws",
-                                      "fused_launches", "exchanges")},
+        "stats": {"leaves": int(tot["leaves"]), "draws": int(tot["draws"]), "edge_draws": int(tot["edge_draws"]),
+                  "sampled_vectors": int(tot["sampled_vectors"]), "resets": int(tot["resets"]),
+                  "gate_apps": int(tot["gate_apps"]), "sweeps": int(tot["sweeps"]),
+                  "fused_launches": int(tot["fused_launches"]), "hbm_GB": tot["hbm_bytes"] / 1e9,
+                  "tree_leaves": info["n_leaves"], "dftt_ops": info["dftt_ops"], "naive_ops": info["naive_ops"],
+                  "rank_leaves": [lb, le]},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         per, cores, desc = cpu_oracle_rate(cfg, args.cpu_seconds)
-        v = per * info["naive_ops"]
-        line["cpu_baseline"] = {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": desc,
-                                "extrapolated": True}
+        line["cpu_baseline"] = {"value": per * info["naive_ops"], "unit": "s", "cores": cores, "kind": "oracle",
+                                "sample": desc, "extrapolated": True}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        comm.free()
+        dist.destroy_process_group()
+
+
+def run_sharded(args, rank, world, local):
+    """Sharded mode: the first --leaves DFS leaves of C5-size states, amplitudes split by
+    global qubits over N ranks (or --shards local shards on one GPU).  A full C5 circuit is ~16
+    GPU-hours, so this line times a leaf prefix and is labelled as such (not the headline)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_04880_b200 as T
+
+    torch.cuda.set_device(local)
+    cfg = W.config(args.config)
+    nz = cfg.noise
+    n, prec = cfg.n, args.precision
+    dt = torch.complex128 if prec == 128 else torch.complex64
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2508_04880_b200 import dist as D
+        comm, _ = D.make_comm(local)
+        nshards = world
+        state = torch.empty(1 << (n - (world.bit_length() - 1)), dtype=dt, device="cuda")
+    else:
+        nshards = args.shards or 2
+        comm = T.Comm.local(nshards)
+        state = torch.empty(1 << n, dtype=dt, device="cuda")
+    t0 = time.perf_counter()
+    tree = T.build_error_tree(n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
+    t_ecm = time.perf_counter() - t0
+    nl = tree.n_leaves
+    per = max(1, args.leaves // max(args.steps, 1)) if args.leaves else 2
+    stream = torch.cuda.current_stream()
+    slots = np.zeros(cfg.shots, dtype=np.uint64)
+    for w in range(args.warmup):
+        T.run_tree(tree, prec, d_state=state, stream=stream, leaf_begin=w, leaf_end=w + 1, comm=comm,
+                   out_slots=slots)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for s in range(args.steps):
+            b = s * per
+            st = T.run_tree(tree, prec, d_state=state, stream=stream, leaf_begin=b, leaf_end=min(nl, b + per),
+                            flags=T.EXEC_CONTINUE if s else 0, comm=comm, out_slots=slots)[1]
+            stats.append(st)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    t_dev = e0.elapsed_time(e1) / 1e3
+    tot = {k: sum(st[k] for st in stats) for k in stats[0]}
+    _, plan = T.run_tree(tree, prec, flags=T.EXEC_PLAN_ONLY, comm=T.Comm.local(nshards))
+    proj = t_ecm + t_dev * (plan["hbm_bytes"] + plan["sample_bytes"]) / max(tot["hbm_bytes"] + tot["sample_bytes"], 1)
+    if rank == 0:
+        print(json.dumps({
+            "metric": f"noisy-sim wall s per circuit ({cfg.name}, sharded x{nshards})", "value": proj, "unit": "s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev * 1e3 / args.steps,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": f"c{prec}",
+            "data": "synthetic", "config": config_dict(cfg, prec, world),
+            "extrapolated": True, "timed_leaves": int(tot["leaves"]), "tree_leaves": nl,
+            "projection": "ECM s + timed device s x (plan bytes / timed bytes)",
+            "gpu_launches": int(tot["launches"]), "clocks": clk.summary(),
+            "stats": {k: tot[k] for k in ("leaves", "resets", "gate_apps", "sweeps", "draws", "exchanges")},
+            "e2e": None}), flush=True)
+    if world > 1:
+        comm.free()
         dist.destroy_process_group()
 
 

@@ -215,6 +215,14 @@ tusq_status tusq_comm_init(const uint8_t id[128], int nranks, int rank, int devi
 tusq_status tusq_comm_init_local(int nshards, int device, tusq_comm **out);
 void tusq_comm_free(tusq_comm *comm);
 
+/* Replica mode, one process per GPU (SURVEY 8(e), P:316 parallel sub-trees): every rank ran its
+ * own DFS leaf ranges into its own host slot array (zeros elsewhere); this sums the arrays of all
+ * ranks in place with one ncclAllReduce on the device (u64, exact: the ranks' slots are
+ * disjoint), so every rank ends with all n slots.  slots: host array of n u64 (in/out).
+ * comm: an NCCL communicator (tusq_comm_init); TUSQ_ERR_INVALID_ARG for a local one.
+ * Synchronizes `stream` before returning. */
+tusq_status tusq_reduce_slots(tusq_comm *comm, uint64_t *slots, uint64_t n, void *stream);
+
 /* Inverse-CDF draws from |amp|^2 of a device state: draw j uses Philox counter
  * (j, leaf_lo, leaf_hi, 0x53000000) keyed by seed, u = (x >> 11) 2^-53, t = u * sum|amp|^2,
  * outcome min{k : C(k) > t}.  d_out: device array of n_draws u64. */

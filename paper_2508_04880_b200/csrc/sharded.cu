@@ -684,6 +684,30 @@ tusq_status tusq_comm_init_local(int nshards, int device, tusq_comm **out)
     return TUSQ_OK;
 }
 
+tusq_status tusq_reduce_slots(tusq_comm *comm, uint64_t *slots, uint64_t n, void *stream)
+{
+    if (!comm || (!slots && n)) return fail(TUSQ_ERR_INVALID_ARG, "NULL argument");
+    if (comm->local) return fail(TUSQ_ERR_INVALID_ARG, "a local communicator has no ranks to reduce over");
+    if (!n) return TUSQ_OK;
+    auto &a = nccl::api();
+    if (!a.ok) return fail(TUSQ_ERR_NCCL, "libnccl.so.2 not available");
+    if (comm->device >= 0 && cudaSetDevice(comm->device) != cudaSuccess) return fail(TUSQ_ERR_CUDA, "cudaSetDevice failed");
+    cudaStream_t st = (cudaStream_t)stream;
+    uint64_t *d = nullptr;
+    if (cudaMallocAsync((void **)&d, n * sizeof(uint64_t), st) != cudaSuccess) return fail(TUSQ_ERR_OOM, "cudaMallocAsync failed");
+    tusq_status rc = TUSQ_OK;
+    std::string err;
+    if (cudaMemcpyAsync(d, slots, n * sizeof(uint64_t), cudaMemcpyHostToDevice, st) != cudaSuccess)
+        rc = fail(TUSQ_ERR_CUDA, "cudaMemcpyAsync (slots in) failed");
+    else if (comm_allreduce_u64(comm, d, n, st, err) != TUSQ_OK)
+        rc = fail(TUSQ_ERR_NCCL, err);
+    else if (cudaMemcpyAsync(slots, d, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = fail(TUSQ_ERR_CUDA, "cudaMemcpyAsync (slots out) failed");
+    cudaFreeAsync(d, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess && rc == TUSQ_OK) rc = fail(TUSQ_ERR_CUDA, "cudaStreamSynchronize failed");
+    return rc;
+}
+
 void tusq_comm_free(tusq_comm *c)
 {
     if (!c) return;

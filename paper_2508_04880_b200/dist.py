@@ -71,12 +71,16 @@ def share_unique_id(group=None, unique_id: Optional[Callable[[], bytes]] = None)
     return bytes(box[0])
 
 
-def make_sharded_comm(device: int, group=None, unique_id: Optional[Callable[[], bytes]] = None):
-    """Sharded mode: one tusq_comm per rank of the torch.distributed group, joined to the
-    library's own NCCL communicator (tusq_comm_init).  Returns (comm, uid bytes)."""
+def make_comm(device: int, group=None, unique_id: Optional[Callable[[], bytes]] = None):
+    """One tusq_comm per rank of the torch.distributed group, joined to the library's own NCCL
+    communicator (tusq_comm_init): the sharded mode's exchanges and the replica
+    mode's slot reduction (tusq_reduce_slots / exec.comm).  Returns (comm, uid bytes)."""
     import torch.distributed as dist
 
     from . import tusq as T
 
     uid = share_unique_id(group, unique_id)
     return T.Comm.nccl(uid, dist.get_world_size(group), dist.get_rank(group), device), uid
+
+
+make_sharded_comm = make_comm

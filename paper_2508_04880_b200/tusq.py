@@ -76,6 +76,7 @@ _sigs = {
     "tusq_comm_unique_id": [_vp],
     "tusq_comm_init": [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
     "tusq_comm_init_local": [C.c_int, C.c_int, C.POINTER(_vp)],
+    "tusq_reduce_slots": [_vp, _u64p, C.c_uint64, _vp],
 }
 for _name, _args in _sigs.items():
     getattr(_lib, _name).argtypes = _args
@@ -257,3 +258,11 @@ def apply_ops(d_state, n: int, precision: int, ops, flags: int = 0, stream=None)
 
 def init_basis(d_state, n: int, precision: int, index: int, re: float = 1.0, im: float = 0.0, stream=None):
     _check(_lib.tusq_init_basis(_ptr(d_state), n, precision, index, re, im, _ptr(stream)), "tusq_init_basis")
+
+
+def reduce_slots(comm: "Comm", slots: np.ndarray, stream=None) -> np.ndarray:
+    """Sum the replica ranks' (disjoint) host slot arrays in place over an NCCL Comm (tusq_reduce_slots)."""
+    if not (isinstance(slots, np.ndarray) and slots.dtype == np.uint64 and slots.flags.c_contiguous):
+        raise ValueError("slots must be a C-contiguous uint64 array")
+    _check(_lib.tusq_reduce_slots(comm.h, slots.ctypes.data_as(_u64p), slots.size, _ptr(stream)), "tusq_reduce_slots")
+    return slots

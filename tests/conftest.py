@@ -20,6 +20,36 @@ def oracle():
     return O
 
 
+class _OracleRuns:
+    """Session cache of full oracle runs (slots, edge flags) and trees per config: the oracle's
+    C2b run replays 7968 dense leaves and several GPU tests compare against it."""
+
+    def __init__(self, O):
+        self.O, self.trees, self.runs = O, {}, {}
+
+    def tree(self, name):
+        if name not in self.trees:
+            from workloads import circuits as W
+            self.trees[name] = self.O.Tree.from_config(W.config(name))
+        return self.trees[name]
+
+    def run(self, name):
+        if name not in self.runs:
+            self.runs[name] = self.tree(name).run()
+        return self.runs[name]
+
+
+@pytest.fixture(scope="session")
+def oracle_runs(oracle):
+    return _OracleRuns(oracle)
+
+
+def edge_budget(draws: int) -> int:
+    """Most edge draws (excluded from slot parity) a c128 slot test may see: a broken edge flag
+    would otherwise make every slot comparison vacuous."""
+    return max(3, draws // 1000)
+
+
 def has_cuda():
     try:
         import torch

@@ -10,6 +10,7 @@ logical order after restoring the canonical layout, so draws are comparable slot
 import numpy as np
 import pytest
 
+from conftest import edge_budget
 from workloads import circuits as W
 
 pytestmark = pytest.mark.gpu
@@ -42,12 +43,13 @@ def _random_cfg(seed, n, n_gates, shots=512):
 
 
 @pytest.mark.parametrize("name,nshards", [("C2a", 2), ("C2a", 8), ("C2b", 2), ("C2b", 4), ("C2b", 8)])
-def test_sharded_slots_match_oracle(T, torch, oracle, name, nshards):
+def test_sharded_slots_match_oracle(T, torch, oracle_runs, name, nshards):
     cfg = W.config(name)
     t = _tree(T, cfg)
     comm = T.Comm.local(nshards)
     slots, stats = T.run_tree(t, 128, comm=comm)
-    ref, edge = oracle.Tree.from_config(cfg).run()
+    ref, edge = oracle_runs.run(name)
+    assert int(edge.sum()) <= edge_budget(cfg.shots)
     bad = (slots != ref) & ~edge
     assert bad.sum() == 0, (int(bad.sum()), int(edge.sum()), stats)
     assert stats["draws"] == cfg.shots and stats["leaves"] == t.n_leaves
@@ -56,11 +58,12 @@ def test_sharded_slots_match_oracle(T, torch, oracle, name, nshards):
 
 
 @pytest.mark.parametrize("name,nshards,prec", [("C2b", 4, 128), ("C2b", 8, 64), ("C3", 2, 128), ("C1", 2, 128)])
-def test_sharded_leaf_amplitudes(T, torch, oracle, name, nshards, prec):
+def test_sharded_leaf_amplitudes(T, torch, oracle_runs, name, nshards, prec):
     # after a DFS range (uncompute + re-anchor + exchanges), the canonical shards = the oracle replay
+    # of the leaf's core (its readout flips relabel draws, reading #7)
     cfg = W.config(name)
     t = _tree(T, cfg)
-    ot = oracle.Tree.from_config(cfg)
+    ot = oracle_runs.tree(name)
     comm = T.Comm.local(nshards)
     nl = t.n_leaves
     rng = np.random.default_rng(5)
@@ -69,7 +72,7 @@ def test_sharded_leaf_amplitudes(T, torch, oracle, name, nshards, prec):
         d = torch.zeros(1 << cfg.n, dtype=dt, device="cuda")
         T.run_tree(t, prec, d_state=d, leaf_begin=max(0, l - 30), leaf_end=l + 1, flags=T.EXEC_NO_SAMPLE, comm=comm)
         torch.cuda.synchronize()
-        err = np.abs(d.cpu().numpy() - ot.replay_leaf(l)).max()
+        err = np.abs(d.cpu().numpy() - ot.replay_leaf_core(l)).max()
         assert err < TOL[prec], (l, err)
 
 
@@ -86,8 +89,9 @@ def test_sharded_random_circuits(T, torch, oracle, n, nshards):
     slots, stats = T.run_tree(t, 128, d_state=d, comm=comm)
     torch.cuda.synchronize()
     ref, edge = ot.run()
+    assert int(edge.sum()) <= edge_budget(cfg.shots)
     assert ((slots != ref) & ~edge).sum() == 0, stats
-    assert np.abs(d.cpu().numpy() - ot.replay_leaf(t.n_leaves - 1)).max() < 1e-10
+    assert np.abs(d.cpu().numpy() - ot.replay_leaf_core(t.n_leaves - 1)).max() < 1e-10
     # the same tree in replica mode gives the same slots
     slots_r, _ = T.run_tree(t, 128)
     assert ((slots != slots_r) & ~edge).sum() == 0

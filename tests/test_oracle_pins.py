@@ -460,3 +460,67 @@ def test_terminal_flips_are_readout_relabels(oracle):
         _, cnt, off = t.leaf(l)
         k, e = oracle.sample_state(t.replay_leaf_core(l), n, 7, l, cnt)
         assert np.array_equal(slots[off:off + cnt], k ^ np.uint64(t.terminal_mask(l)))
+
+
+# ------------------------------------------------------------------ sparse replay (oracle/sparse.py)
+def test_sparse_replay_matches_dense_oracle(oracle):
+    # the dict-based replay equals the dense oracle's replay (same definition, Eq. 1) on
+    # random circuits over the full gate set with random frozen Paulis, forward and inverse gates
+    from oracle import sparse as SP
+    rng = np.random.default_rng(31)
+    for trial in range(30):
+        n = int(rng.integers(2, 8))
+        ops = W.random_circuit(rng, n, int(rng.integers(5, 60)))
+        L = len(ops)
+        triples = sorted({(int(rng.integers(0, L + 1)), int(rng.integers(n)), int(rng.integers(1, 4)))
+                          for _ in range(int(rng.integers(0, 6)))})
+        dense = oracle.replay(n, ops, triples)
+        sp = SP.replay(ops, triples)
+        got = np.zeros(1 << n, dtype=complex)
+        for i, a in sp.items():
+            got[i] = a
+        assert np.abs(got - dense).max() < 1e-13, trial
+        # inverse gates: G^-1 G = I on a random basis state
+        i0 = int(rng.integers(1 << n))
+        st = {i0: 1.0 + 0j}
+        for g in ops:
+            st = SP.apply_gate(st, g)
+        for g in reversed(ops):
+            st = SP.apply_gate(st, g, inverse=True)
+        back = np.zeros(1 << n, dtype=complex)
+        for i, a in st.items():
+            back[i] = a
+        ref = np.zeros(1 << n, dtype=complex)
+        ref[i0] = 1
+        assert np.abs(back - ref).max() < 1e-12
+
+
+def test_sparse_replay_adder_closed_form():
+    # noiseless Cuccaro adder (reading #13): a single basis state with amplitude 1; with the
+    # 1e-14 rounding-residue cut the support stays one entry through all 498 gates at 30 qubits
+    from oracle import sparse as SP
+    for k in (1, 3, 11, 14):
+        n, ops = W.adder(k)
+        st = SP.replay(ops, [], drop_below=1e-14)
+        assert list(st) == [W.adder_expected_output(k)]
+        assert abs(st[W.adder_expected_output(k)] - 1) < 1e-13
+
+
+def test_sparse_sampler_matches_dense_sampler(oracle):
+    # oracle/sparse.sample over the nonzero entries == or_sample_state over the dense vector
+    # (zeros leave the compensated CDF unchanged), draw for draw incl. edge flags
+    from oracle import sparse as SP
+    rng = np.random.default_rng(12)
+    for trial in range(20):
+        n = int(rng.integers(1, 11))
+        N = 1 << n
+        st = np.zeros(N, dtype=complex)
+        nz = rng.choice(N, size=int(rng.integers(1, min(N, 40) + 1)), replace=False)
+        st[nz] = rng.normal(size=len(nz)) + 1j * rng.normal(size=len(nz))
+        st /= np.linalg.norm(st)
+        seed, leaf, nd = int(rng.integers(1 << 40)), int(rng.integers(1 << 33)), int(rng.integers(1, 300))
+        ref, redge = oracle.sample_state(st, n, seed, leaf, nd, 1e-3)
+        sp = {int(i): complex(st[i]) for i in nz}
+        got, gedge = SP.sample(sp, seed, leaf, nd, 1e-3)
+        assert np.array_equal(np.array(got, dtype=np.uint64), ref), trial
+        assert np.array_equal(np.array(gedge), redge), trial
