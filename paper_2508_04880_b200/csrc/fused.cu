@@ -21,6 +21,8 @@
 //   - a reset to a basis state (K7) is fused into the first sweep (no load);
 //   - the last sweep before sampling can emit per-4096-block |amp|^2 sums (K6 epilogue).
 #include <algorithm>
+#include <array>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -112,16 +114,26 @@ struct GRec {
     uint16_t _pad;
 };
 
-enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4 };
+enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8 };
+constexpr int NCH = 4;             // 8-bit chunks of the tile index (n <= TB + 8 * NCH = 44 fused)
 
+// Qubit layout: the state may be stored with its qubits permuted (logical qubit q at physical bit
+// position pi(q)); logical index l lives at physical address pi(l ^ xm).  A sweep reads with the
+// layout pi_in and writes with pi_out, chosen by the planner so that the NEXT group's 12 tile
+// qubits sit at physical positions 0..11 -- every tile read after the first group of a transition
+// is one contiguous 64 KiB block; transitions begin and end in the
+// identity layout.
 struct Params {
-    uint64_t xm_load, xm_store;   // physical = logical ^ mask at load / at store
+    uint64_t xm_load, xm_store;   // logical X-relabel mask at load / at store (outer bits only)
+    uint64_t xin, xout;           // xm_store in the read / write layout
     uint64_t init_index;          // F_INIT: virtual memory holds init amp at physical init_index
     double init_re, init_im;
     double scale_re, scale_im;
     uint64_t ntiles;
-    uint32_t flags, nphase, ngate, _pad2;
-    uint8_t qs[TB];               // tile-local bit b <-> global qubit qs[b] (ascending)
+    uint32_t flags, nphase, ngate, nout;
+    uint8_t qs[TB];               // tile-local bit b <-> logical qubit qs[b] (tile-local order = read order)
+    uint8_t pin[TB], pout[TB];    // physical read / write position of tile-local bit b
+    uint8_t oo[64], ol[64];       // tile-index bit k (outer qubits in read order): write / logical position
     uint32_t rx;                  // register bits where xm_load is set (folded into gl, kept 0)
     uint16_t mloc;                // tile-local bits of xm_load (applied when copying to shared memory)
     uint16_t last_xpose;          // record index of the last transpose (0xFFFF: none)
@@ -131,8 +143,8 @@ struct Params {
                                   // layout -> one 2x-wide store per pair
     uint32_t st_odd;              // bit r: register r holds the odd one of its pair
     uint64_t regm_load;           // global mask of the phase-0 register qubits
-    uint64_t outer;               // mask of the outer (non-tile) qubits
-    uint64_t dstep;               // pdep(gridDim.x * NG, outer): next tile of the same group
+    uint64_t outer;               // read-layout mask of the outer (non-tile) positions
+    uint64_t dstep;               // pdep(gridDim.x * NG, outer): next tile of the same group (read layout)
     uint64_t dissue[NG];          // pdep(T(j + NBUF) - T(j), outer) for a tile j of group g
     // gj, gs, sj and the phases' so / so_out are BYTE offsets at launch (element offsets while
     // the host plans): the kernel adds them to byte pointers with no index scaling
@@ -548,23 +560,27 @@ __device__ __forceinline__ void cp_async(void *smem, const void *gmem)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-__device__ __forceinline__ uint64_t tile_base(uint64_t T, const uint8_t (&qs)[TB])
+// tile bases in the read layout: the tile index deposited into the outer positions
+__device__ __forceinline__ uint64_t pdep_outer(uint64_t T, uint64_t m)
 {
-    uint64_t base = T;
-#pragma unroll
-    for (int b = 0; b < TB; ++b) base = ins0(base, qs[b]);
-    return base;
+    uint64_t o = 0;
+    for (uint64_t b = 1; m; m &= m - 1) {
+        if (T & b) o |= m & (~m + 1);
+        b <<= 1;
+    }
+    return o;
 }
 
-// Copy tile T (physical tile base = logical base ^ xm_store) into shared memory in LOGICAL
-// tile order: thread tid copies physical local indices p = tid + NT*j (coalesced: lanes 0-7 run
-// over qubits 0,1,2), to slot swz(p ^ mloc).
+// Copy a tile into shared memory in LOGICAL tile order: thread tid copies tile-local indices
+// p = tid + NT*j from their read-layout addresses (tile-local bits are in read-position order, so
+// a warp copies 512 contiguous bytes when the tile's qubits sit at physical 0..11), to slot
+// swz(p ^ mloc).
 template <typename V>
 __device__ __forceinline__ void prefetch_tile(V *sm, const V *psi, uint64_t tbase, const Params &P, uint64_t gt,
                                               uint32_t tid)
 {
-    // tbase: the tile's logical base (outer bits); all offsets below are in bytes
-    const char *src = reinterpret_cast<const char *>(psi + ((tbase ^ P.xm_store) + gt));
+    // tbase: the tile's base in the read layout (outer positions); all offsets below are in bytes
+    const char *src = reinterpret_cast<const char *>(psi + ((tbase ^ P.xin) + gt));
     char *dst = reinterpret_cast<char *>(sm);
     const uint32_t st = swz(tid ^ P.mloc) * (uint32_t)sizeof(V);
 #pragma unroll
@@ -680,39 +696,69 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
         uint32_t *dst = reinterpret_cast<uint32_t *>(gsm);
         for (uint32_t i = threadIdx.x; i < NR * NT / 2; i += NT * NG) dst[i] = src[i];
     }
+    // tile index -> write-layout / logical base: one table per 8-bit chunk of the tile index
+    uint64_t(*tabo)[256] = reinterpret_cast<uint64_t(*)[256]>(gsm + NR * NT);
+    uint64_t(*tabl)[256] = tabo + NCH;
+    const bool need_l = P.flags & (F_LBASE | F_INIT);
+    for (uint32_t i = threadIdx.x; i < NCH * 256; i += NT * NG) {
+        const uint32_t c = i >> 8, v = i & 255u;
+        uint64_t o = 0, l = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < 8; ++b) {
+            const uint32_t k = c * 8 + b;
+            if (((v >> b) & 1u) && k < P.nout) {
+                o |= 1ull << P.oo[k];
+                l |= 1ull << P.ol[k];
+            }
+        }
+        tabo[c][v] = o;
+        tabl[c][v] = l;
+    }
     if (threadIdx.x == 0) {
         for (int b = 0; b < NBUF; ++b) mbar_init(&mbar[b], NT);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // global offset of this thread's copy slot: tile-local bits 0..NTB-1 = tid (tile independent)
+    auto lookup = [&](uint64_t(*tab)[256], uint64_t T) {
+        uint64_t o = tab[0][T & 255u];
+#pragma unroll
+        for (int c = 1; c < NCH; ++c) o |= tab[c][(T >> (8 * c)) & 255u];
+        return o;
+    };
+    // read-layout offset of this thread's copy slot: tile-local bits 0..NTB-1 = tid (tile independent)
     uint64_t gt = 0;
 #pragma unroll
-    for (int b = 0; b < NTB; ++b) gt |= (uint64_t)((tid >> b) & 1u) << P.qs[b];
+    for (int b = 0; b < NTB; ++b) gt |= (uint64_t)((tid >> b) & 1u) << P.pin[b];
     // the first NBUF tiles: tile j is issued by group j % NG
-    for (uint64_t j = grp; j < NBUF; j += NG) issue_tile(smbase, mbar, psi, j, tile_base(cta_tile(j), P.qs), P, gt, tid, init);
+    for (uint64_t j = grp; j < NBUF; j += NG)
+        issue_tile(smbase, mbar, psi, j, pdep_outer(cta_tile(j), P.outer), P, gt, tid, init);
     V a[NR];
-    // logical tile base: the tile index deposited into the outer (non-tile) qubit positions
-    uint64_t base = tile_base(cta_tile(grp), P.qs);
+    // thread parts of the phase-0 logical index (predicates, init) and of the last phase's write address
+    uint64_t gthr0 = 0, gthr_st = 0;
+    {
+        const Phase &p0 = P.ph[0], &pl = P.ph[P.nphase - 1];
+#pragma unroll
+        for (int q = 0; q < NTB; ++q) {
+            gthr0 |= (uint64_t)((tid >> q) & 1u) << P.qs[p0.tl[q]];
+            gthr_st |= (uint64_t)((tid >> q) & 1u) << P.pout[pl.tl[q]];
+        }
+    }
+    // read-layout tile base: the tile index deposited into the outer positions (stepped in place)
+    uint64_t base = pdep_outer(cta_tile(grp), P.outer);
     const uint64_t dissue = P.dissue[grp];
     for (uint64_t j = grp;; j += NG, base = dep_add(base, P.dstep, P.outer)) {
         const uint64_t T = cta_tile(j);
         if (T >= P.ntiles) break;
         V *sm = smbase + (size_t)(j % NBUF) * (1u << TB);
         char *smb = reinterpret_cast<char *>(sm);
-
-        // ---- phase 0 layout: global offset of this thread's bits; register offsets come from
-        // the parameter block (constant bank), added to one base pointer
-        uint64_t gthr = 0;
-        {
-            const Phase &p0 = P.ph[0];
-#pragma unroll
-            for (int q = 0; q < NTB; ++q) gthr |= (uint64_t)((tid >> q) & 1u) << P.qs[p0.tl[q]];
-        }
+        const uint64_t bout = lookup(tabo, T);
+        const uint64_t blog = need_l ? lookup(tabl, T) : 0;
+        const uint64_t gthr = gthr0;
         mbar_wait(&mbar[j % NBUF], (uint32_t)((j / NBUF) & 1));
         if (init) {
             // the same addressing as a load, from a virtual memory holding init at init_index
-            const uint64_t lt = ((base | gthr) ^ P.xm_load) & ~P.regm_load;
+            // (a reset group reads the identity layout: logical = physical positions)
+            const uint64_t lt = ((blog | gthr) ^ P.xm_load) & ~P.regm_load;
 #pragma unroll
             for (int r = 0; r < NR; ++r) {
                 const bool hit = (lt + P.gl[r]) == P.init_index;
@@ -742,9 +788,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
         // join at a single loop header with the amplitudes in one canonical register set (nested
         // phase/gate loops made ptxas copy every amplitude at each gate iteration).
         uint32_t ph = 0;
-        uint64_t lbase = base;
-#pragma unroll
-        for (int q = 0; q < NTB; ++q) lbase |= (uint64_t)((tid >> q) & 1u) << P.qs[P.ph[0].tl[q]];
+        uint64_t lbase = blog | gthr0;   // logical index bits of this thread (thread + outer) for predicates
         // records are fetched as one 64-bit constant load, one record ahead (the fetch -> decode
         // -> branch chain was the top stall in ncu's source view; a shared-memory copy fetched by
         // a volatile load at the top of the iteration measured ~6 % slower)
@@ -791,9 +835,11 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
                 TQ_LD(24) TQ_LD(25) TQ_LD(26) TQ_LD(27) TQ_LD(28) TQ_LD(29) TQ_LD(30) TQ_LD(31)
 #undef TQ_LD
                 // logical index bits of this thread (thread + outer bits) for predicates
-                lbase = base;
+                if (need_l) {
+                    lbase = blog;
 #pragma unroll
-                for (int q = 0; q < NTB; ++q) lbase |= (uint64_t)((tid >> q) & 1u) << P.qs[cur.tl[q]];
+                    for (int q = 0; q < NTB; ++q) lbase |= (uint64_t)((tid >> q) & 1u) << P.qs[cur.tl[q]];
+                }
                 if (gi == P.last_xpose) {   // the buffer is free until tile j + NBUF: hand it over
                     named_bar(bar);
                     issue_tile(smbase, mbar, psi, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
@@ -801,11 +847,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
             }
         }
 
-        // ---- store with the last layout
-        const Phase &last = P.ph[P.nphase - 1];
-        gthr = 0;
-#pragma unroll
-        for (int q = 0; q < NTB; ++q) gthr |= (uint64_t)((tid >> q) & 1u) << P.qs[last.tl[q]];
+        // ---- store with the last phase's thread layout, into the write layout
         if (P.flags & F_SCALE) {
             const R sr = (R)P.scale_re, si = (R)P.scale_im;
             if (si == R(0)) {
@@ -816,8 +858,8 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
                 for (int r = 0; r < NR; ++r) cmul_ip(a[r], sr, si);
             }
         }
-        // xm_store has no tile bits: register offsets are additive
-        V *q0 = psi + ((base | gthr) ^ P.xm_store);
+        // xout has no tile bits: register offsets are additive
+        V *q0 = psi + ((bout | gthr_st) ^ P.xout);
         if (P.st_pair) {
             switch (P.st_pair) {
 #define TQ_SP(v) case v: if constexpr (v < NR) store_pairs<v>(q0, a, P); break;
@@ -847,7 +889,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
                 double t = 0.0;
 #pragma unroll
                 for (int w = 0; w < NT / 32; ++w) t += red[grp][w];
-                sums[(base ^ P.xm_store) >> TB] = t;
+                sums[(bout ^ P.xout) >> TB] = t;   // (F_SUMS: identity write layout, tile {0..11})
             }
             named_bar(bar);
         }
@@ -988,7 +1030,7 @@ void execute_unfused(const std::vector<Op> &ops, Ctx &ctx)
 }
 
 FusedPlanner::FusedPlanner(uint32_t n, int prec)
-    : n_(n), prec_(prec), tile_bits_(TB), enabled_(n >= (uint32_t)TB)
+    : n_(n), prec_(prec), tile_bits_(TB), enabled_(n >= (uint32_t)TB && n <= (uint32_t)(TB + 8 * NCH))
 {
 }
 
@@ -999,10 +1041,14 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
 {
     // strict: every qubit an op touches (controls, diagonals) must join the tile, so whole runs
     // stay in registers and fold; otherwise they join only while there is room
-    const uint64_t low = 7;   // qubits 0,1,2 are always tile qubits
+    // Tile capacity.  Every group after the first reads a layout in which its own tile qubits sit
+    // at physical positions 0..11 (see FusedPlanner::execute_ex), so any 12 qubits make a
+    // contiguous tile; the first group reads the identity layout, so it keeps qubits 0,1,2
+    // (128-byte runs) and up to 9 others.
+    uint64_t low = 7;
+    int hi_cap = TB - 3;
     // tile qubits a group may claim beyond 0-2 (default all 9; fewer leave fillers 3, 4... in the
     // tile, i.e. longer contiguous runs per tile row, at the price of more sweeps)
-    constexpr int hi_cap = TB - 3;
     std::vector<Group> groups;
     Group g;
     uint64_t touched = 0;
@@ -1032,6 +1078,7 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
             if (!drop[i]) kept.push_back(g.ops[i]);
         g.ops.swap(kept);
         if (!g.ops.empty() || g.xb || g.xa) groups.push_back(g);
+        if (!groups.empty()) { low = 0; hi_cap = TB; }
         g = Group();
         touched = 0;
     };
@@ -1201,21 +1248,46 @@ static bool diag_of(const Op &o, double d[4])
     }
 }
 
-static void build_params(const Group &G, uint32_t n, Built &B)
+// tile: the group's 12 logical tile qubits; lin / lout: physical position of every logical qubit
+// in the read / write layout
+static void build_params(const Group &G, uint32_t n, Built &B, uint64_t tile, const uint8_t *lin,
+                         const uint8_t *lout)
 {
     Params &P = B.P;
     memset(&P, 0, sizeof(P));
-    // tile qubits: 0,1,2 + required + fillers (lowest unused)
-    uint64_t tile = G.tilemask | 7ull;
-    for (uint32_t q = 0; __builtin_popcountll(tile) < TB && q < n; ++q) tile |= bit(q);
     B.tile = tile;
     uint8_t loc[64];
     memset(loc, 0xff, sizeof(loc));
     {
-        int b = 0;
+        // tile-local bits in read order: tile-local index = read offset when the tile is contiguous
+        std::vector<uint32_t> tq;
         for (uint32_t q = 0; q < n; ++q)
-            if (tile & bit(q)) { P.qs[b] = (uint8_t)q; loc[q] = (uint8_t)b; ++b; }
+            if (tile & bit(q)) tq.push_back(q);
+        std::sort(tq.begin(), tq.end(), [&](uint32_t a, uint32_t b) { return lin[a] < lin[b]; });
+        for (int b = 0; b < TB; ++b) {
+            P.qs[b] = (uint8_t)tq[b];
+            P.pin[b] = lin[tq[b]];
+            P.pout[b] = lout[tq[b]];
+            loc[tq[b]] = (uint8_t)b;
+        }
+        // tile index bits: the outer qubits in read order
+        std::vector<uint32_t> oq;
+        for (uint32_t q = 0; q < n; ++q)
+            if (!(tile & bit(q))) oq.push_back(q);
+        std::sort(oq.begin(), oq.end(), [&](uint32_t a, uint32_t b) { return lin[a] < lin[b]; });
+        P.nout = (uint32_t)oq.size();
+        for (size_t k = 0; k < oq.size(); ++k) {
+            P.oo[k] = lout[oq[k]];
+            P.ol[k] = (uint8_t)oq[k];
+            P.outer |= bit(lin[oq[k]]);
+        }
     }
+    // lane preference: tile bits by write position (the store's lanes 0-2 want write positions
+    // 0-2); lanes 0-2 of every layout also need distinct (bit mod 3) classes -- the swizzle maps
+    // tile bit b to bank group bit (b mod 3), so that keeps the quarter-warps conflict-free
+    uint8_t lp[TB];
+    for (int b = 0; b < TB; ++b) lp[b] = (uint8_t)b;
+    std::sort(lp, lp + TB, [&](uint8_t a, uint8_t b) { return P.pout[a] < P.pout[b]; });
     // register-need sequence
     // needq: the qubit an op must have in a register (exchange target); ctrlq: a CX control that
     // also triggers a phase switch when it is a tile qubit outside the registers -- a register
@@ -1251,12 +1323,11 @@ static void build_params(const Group &G, uint32_t n, Built &B)
             uint32_t q = __builtin_ctzll(m);
             if (!(have & bit(q))) { have |= bit(q); rs.push_back(q); }
         }
-        for (int pass = 0; pass < 2 && rs.size() < (size_t)RB; ++pass)
-            for (uint32_t b = (pass ? 3 : 0); b < (uint32_t)TB && rs.size() < (size_t)RB; ++b) {
-                uint32_t q = P.qs[b];
-                if (pass == 0 && b < 3) continue;
-                if (!(have & bit(q))) { have |= bit(q); rs.push_back(q); }
-            }
+        // then the tile bits least wanted as store lanes (largest write positions first)
+        for (int i = TB - 1; i >= 0 && rs.size() < (size_t)RB; --i) {
+            const uint32_t q = P.qs[lp[i]];
+            if (!(have & bit(q))) { have |= bit(q); rs.push_back(q); }
+        }
         return rs;
     };
     auto make_phase = [&](const std::vector<uint32_t> &rs, uint16_t g0) {
@@ -1265,19 +1336,20 @@ static void build_params(const Group &G, uint32_t n, Built &B)
         ph.g0 = g0;
         uint32_t rmask = 0;
         for (int k = 0; k < RB; ++k) { ph.rl[k] = loc[rs[k]]; rmask |= 1u << ph.rl[k]; }
-        // lanes 0-2: tile bits 0-2 unless they are register bits (then the lowest free bit >= 3),
-        // lanes 3-4 and warps 0-1: the remaining bits ascending
+        // lanes 0-2: the non-register tile bits of smallest write position with distinct
+        // (b mod 3) classes; lanes 3-4: the next by write position; warps: the rest ascending
         uint32_t used = rmask;
         int tj = 0;
-        for (uint32_t b = 0; b < 3; ++b) {
-            uint32_t pick = b;
-            if (rmask & (1u << b)) {
-                pick = 3;
-                while (used & (1u << pick)) ++pick;
-            }
-            used |= 1u << pick;
-            ph.tl[tj++] = (uint8_t)pick;
+        uint32_t cls = 0;
+        for (int i = 0; i < TB && tj < 3; ++i) {
+            const uint32_t b = lp[i];
+            if ((used >> b) & 1u || (cls >> (b % 3)) & 1u) continue;
+            used |= 1u << b;
+            cls |= 1u << (b % 3);
+            ph.tl[tj++] = (uint8_t)b;
         }
+        for (int i = 0; i < TB && tj < 5; ++i)
+            if (!((used >> lp[i]) & 1u)) { used |= 1u << lp[i]; ph.tl[tj++] = lp[i]; }
         for (uint32_t b = 0; b < (uint32_t)TB && tj < NTB; ++b)
             if (!(used & (1u << b))) { used |= 1u << b; ph.tl[tj++] = (uint8_t)b; }
         for (int r = 0; r < NR; ++r) {
@@ -1777,12 +1849,23 @@ static void build_params(const Group &G, uint32_t n, Built &B)
     B.prm_used = (prm.size() + 1) & ~(size_t)1;   // the gather table starts 16-byte aligned
 }
 
+// dynamic shared memory of k_fused: NBUF tile buffers, the gather table, the tile-index tables
+static size_t smem_bytes(int prec)
+{
+    return (size_t)NBUF * (1 << TB) * (prec == 128 ? 16 : 8) + NR * NT * 2 + 2 * NCH * 256 * sizeof(uint64_t);
+}
+
 static int blocks_per_sm(int prec)
 {
-    static int occ[2] = {0, 0};
-    int &o = occ[prec == 128 ? 1 : 0];
+    // one-time per device and precision (the attribute is per device); concurrent first calls
+    // compute the same value
+    static std::atomic<int> occ[64][2];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::atomic<int> &slot = occ[dev & 63][prec == 128 ? 1 : 0];
+    int o = slot.load(std::memory_order_relaxed);
     if (!o) {
-        size_t smem = (size_t)NBUF * (1 << TB) * (prec == 128 ? 16 : 8) + NR * NT * 2;
+        const size_t smem = smem_bytes(prec);
         if (prec == 128) {
             cudaFuncSetAttribute(k_fused<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused<double>, NT * NG, smem);
@@ -1791,6 +1874,7 @@ static int blocks_per_sm(int prec)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused<float>, NT * NG, smem);
         }
         if (o < 1) o = 1;
+        slot.store(o, std::memory_order_relaxed);
     }
     return o;
 }
@@ -1841,6 +1925,47 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     }
     if (!scratch_) scratch_ = std::make_shared<PlanScratch>();
     Built &B = scratch_->B;
+    // ---- tiles and layouts of the launched groups.  The transition
+    // starts and ends in the identity layout.  Group k >= 1 reads the layout the group before it
+    // wrote: its own 12 tile qubits at physical 0..11 (a contiguous 64 KiB tile), ordered
+    // [shared with group k-1][new], then group k-1's other tile qubits right above them (a
+    // compact write footprint for group k-1), then the rest ascending.  Fillers of a middle group
+    // come from the previous group's tile first (longer write runs for it).
+    std::vector<size_t> launched;
+    {
+        bool pi = pending_init;
+        for (size_t gi = 0; gi < groups.size(); ++gi)
+            if (!groups[gi].ops.empty() || pi) { launched.push_back(gi); pi = false; }
+    }
+    const size_t NLG = launched.size();
+    std::vector<uint64_t> tiles(NLG);
+    for (size_t k = 0; k < NLG; ++k) {
+        uint64_t t = groups[launched[k]].tilemask;
+        auto fill = [&](uint64_t from) {
+            for (uint64_t m = from; m && __builtin_popcountll(t) < TB; m &= m - 1) t |= m & (~m + 1);
+        };
+        if (k > 0 && k + 1 < NLG) fill(tiles[k - 1]);
+        fill(n_ >= 64 ? ~0ull : (1ull << n_) - 1);   // then the lowest unused qubits
+        tiles[k] = t;
+    }
+    std::vector<std::array<uint8_t, 64>> lay(NLG + 1);
+    for (size_t k = 0; k <= NLG; ++k) {
+        auto &L = lay[k];
+        if (k == 0 || k == NLG) {
+            for (uint32_t q = 0; q < 64; ++q) L[q] = (uint8_t)q;
+            continue;
+        }
+        const uint64_t a = tiles[k - 1], b = tiles[k], all = n_ >= 64 ? ~0ull : (1ull << n_) - 1;
+        uint8_t pos = 0;
+        for (uint64_t part : {a & b, b & ~a, a & ~b, all & ~(a | b)})
+            for (uint64_t m = part; m; m &= m - 1) L[__builtin_ctzll(m)] = pos++;
+    }
+    auto permute = [&](uint64_t x, const std::array<uint8_t, 64> &L) {
+        uint64_t o = 0;
+        for (; x; x &= x - 1) o |= bit(L[__builtin_ctzll(x)]);
+        return o;
+    };
+    size_t lk = 0;   // launched-group counter
     for (size_t gi = 0; gi < groups.size(); ++gi) {
         const Group &G = groups[gi];
         if (G.ops.empty() && !pending_init) {   // pure relabel
@@ -1848,11 +1973,14 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             continue;
         }
         // loads go through shared memory (always coalesced): no load-layout phase needed
-        build_params(G, n_, B);
+        build_params(G, n_, B, tiles[lk], lay[lk].data(), lay[lk + 1].data());
         Params &P = B.P;
         uint64_t m_load = (pending_init ? 0 : xmask_) ^ G.xb;
         P.xm_load = m_load;
         P.xm_store = m_load & ~B.tile;
+        P.xin = permute(P.xm_store, lay[lk]);
+        P.xout = permute(P.xm_store, lay[lk + 1]);
+        ++lk;
         {
             const Phase &f = P.ph[0], &l = P.ph[P.nphase - 1];
             P.regm_load = 0;
@@ -1861,17 +1989,18 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 P.regm_load |= bit(P.qs[f.rl[k]]);
                 if (m_load & bit(P.qs[f.rl[k]])) P.rx |= 1u << k;
             }
-            auto goff = [&](const Phase &ph, uint32_t pat) {
+            auto goff = [&](const Phase &ph, uint32_t pat, const uint8_t *posn) {
                 uint64_t o = 0;
                 for (int k = 0; k < RB; ++k)
-                    if (pat & (1u << k)) o |= bit(P.qs[ph.rl[k]]);
+                    if (pat & (1u << k)) o |= bit(posn[ph.rl[k]]);
                 return o;
             };
-            // register r loads physical pattern pin0[r] ^ rx (mask fix-up + absorbed permutation);
-            // register s is stored at the pattern pout_last[s]
+            // register r loads pattern pin0[r] ^ rx (mask fix-up + absorbed permutation; logical
+            // positions: only an init group uses gl, and it reads the identity layout); register s
+            // is stored at the pattern pout_last[s], in the write layout
             for (int r = 0; r < NR; ++r) {
-                P.gl[r] = goff(f, (uint32_t)B.pin0[r] ^ P.rx);
-                P.gs[r] = goff(l, B.pout_last[r]);
+                P.gl[r] = goff(f, (uint32_t)B.pin0[r] ^ P.rx, P.qs);
+                P.gs[r] = goff(l, B.pout_last[r], P.pout);
             }
             P.rx = 0;
             // paired stores when qubit 0 is a register bit of the last layout
@@ -1892,7 +2021,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             for (int j = 0; j < NR; ++j) {
                 uint64_t o = 0;
                 for (int k = 0; k < RB; ++k)
-                    if (j & (1 << k)) o |= bit(P.qs[NTB + k]);
+                    if (j & (1 << k)) o |= bit(P.pin[NTB + k]);
                 P.gj[j] = o;
                 P.sj[j] = (uint16_t)swz((uint32_t)j << NTB);
             }
@@ -1942,6 +2071,10 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         }
         P.ntiles = 1ull << (n_ - TB);
         P.flags = 0;
+        for (uint32_t i = 0; i < P.ngate; ++i) {   // records that read the logical index
+            const uint16_t c = P.g[i].code;
+            if ((c >= C_TX && c <= C_TPH) || (c >= C_TDK && c < C_N)) P.flags |= F_LBASE;
+        }
         if (pending_init) {
             P.flags |= F_INIT;
             P.init_index = init->index;
@@ -1964,12 +2097,11 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         if (!ctx.dry) {
             int bps = blocks_per_sm(prec_);
             uint64_t grid = std::min<uint64_t>((P.ntiles + NG - 1) / NG, (uint64_t)device_sm_count() * bps);
-            size_t smem = (size_t)NBUF * (1 << TB) * (prec_ == 128 ? 16 : 8) + NR * NT * 2;
-            // incremental tile bases (deposited steps) and byte offsets for the kernel
-            P.outer = ((n_ == 64 ? ~0ull : (1ull << n_) - 1)) & ~B.tile;
+            const size_t smem = smem_bytes(prec_);
+            // incremental tile bases (deposited steps, read layout) and byte offsets for the kernel
             auto pdep = [&](uint64_t x) {
                 uint64_t o = 0;
-                for (uint32_t q = 0; q < n_ && x; ++q)
+                for (uint32_t q = 0; q < 64 && x; ++q)
                     if (P.outer & bit(q)) { o |= (x & 1) << q; x >>= 1; }
                 return o;
             };

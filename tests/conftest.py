@@ -38,6 +38,26 @@ class _OracleRuns:
             self.runs[name] = self.tree(name).run()
         return self.runs[name]
 
+    def sparse_run(self, name):
+        """Full-run slots of an Adder config from the oracle's sparse replay (oracle/sparse.py,
+        pinned to the dense oracle): each leaf's core replayed, sampled, XORed with its readout mask."""
+        key = ("sparse", name)
+        if key not in self.runs:
+            import numpy as np
+            from oracle import sparse as SP
+            from workloads import circuits as W
+            cfg = W.config(name)
+            ot = self.tree(name)
+            ref = np.zeros(cfg.shots, dtype=np.uint64)
+            edge = np.zeros(cfg.shots, dtype=bool)
+            for l in range(ot.n_leaves):
+                tr, cnt, off = ot.leaf(l)
+                psi = SP.replay(cfg.ops, SP.core_triples(tr, len(cfg.ops)), drop_below=1e-14)
+                k, e = SP.sample(psi, cfg.seed, l, cnt, 1e-9, ot.terminal_mask(l))
+                ref[off:off + cnt], edge[off:off + cnt] = k, e
+            self.runs[key] = (ref, edge)
+        return self.runs[key]
+
 
 @pytest.fixture(scope="session")
 def oracle_runs(oracle):

@@ -303,12 +303,7 @@ def test_c3_all_slots(T, torch, oracle_runs):
     cfg = W.config("C3")
     t = _tree(T, cfg)
     slots, stats = T.run_tree(t, 128)
-    ot = oracle_runs.tree("C3")
-    ref = np.zeros(cfg.shots, dtype=np.uint64)
-    edge = np.zeros(cfg.shots, dtype=bool)
-    for l in range(ot.n_leaves):
-        psi, cnt, off, mask = _sparse_leaf(ot, cfg, l)
-        ref[off:off + cnt], edge[off:off + cnt] = _sparse_slots(ot, cfg, l, psi, cnt, mask)
+    ref, edge = oracle_runs.sparse_run("C3")
     _check_slots(slots, ref, edge, cfg.shots)
     assert stats["draws"] == cfg.shots
 

@@ -55,7 +55,7 @@ def _worker(rank, world, port, name, out_dir, real=False):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["C2a", "C3"])
-def test_gloo_world2_real_run_tree(tmp_path, oracle, name):
+def test_gloo_world2_real_run_tree(tmp_path, oracle_runs, name):
     # both ranks run the real tusq_run_tree on cuda:0 over their tusq_tree_partition ranges; the gloo
     # SUM of the disjoint slot arrays equals the single-rank library run and the oracle (non-edge)
     port = _free_port()
@@ -70,7 +70,7 @@ def test_gloo_world2_real_run_tree(tmp_path, oracle, name):
     tree = T.build_error_tree(cfg.n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
     single, _ = T.run_tree(tree, 128)
     assert np.array_equal(s0, single)
-    ref, edge = oracle.Tree.from_config(cfg).run()
+    ref, edge = oracle_runs.run(name) if name != "C3" else oracle_runs.sparse_run(name)
     assert int(edge.sum()) <= max(3, cfg.shots // 1000)
     assert ((s0 != ref) & ~edge).sum() == 0
 
