@@ -77,8 +77,26 @@ typedef struct { uint32_t kind, q0, q1, _pad; double theta; } tusq_op;
  *   p1     depolarizing (1-p, p/3, p/3, p/3) after every 1q gate on its qubit,
  *   p2     depolarizing after every 2q gate on EACH of its two qubits,
  *   p_meas X flip before readout on every qubit.
- * A channel with p = 0 attaches no noise site. */
-typedef struct { double p1, p2, p_meas; uint32_t flags, _pad; } tusq_noise;
+ * With flags & TUSQ_NOISE_PAULI the three site classes instead carry general Pauli channels
+ * (Eq. 2: rho -> (1 - pX - pY - pZ) rho + pX X rho X + pY Y rho Y + pZ Z rho Z), given
+ * as (pX, pY, pZ) in pauli1 / pauli2 / pauli_meas -- e.g. the Pauli-twirled decoherence of
+ * tusq_twirl_decoherence, or a depolarizing channel composed with it.  Every p in [0, 1] and each
+ * triple's sum <= 1, else TUSQ_ERR_INVALID_ARG.  A channel whose probabilities are all 0 attaches
+ * no noise site.  Integer thresholds t_P = round(p_P 2^32), t_I = 2^32 - (t_X + t_Y + t_Z). */
+#define TUSQ_NOISE_PAULI 0x1u
+typedef struct {
+    double p1, p2, p_meas;
+    uint32_t flags, _pad;
+    double pauli1[3];       /* TUSQ_NOISE_PAULI: (pX, pY, pZ) after every 1q gate */
+    double pauli2[3];       /*                   on each qubit of every 2q gate */
+    double pauli_meas[3];   /*                   right before readout, every qubit */
+} tusq_noise;
+
+/* Pauli-twirling approximation of decoherence for an idle time t (Eq. 2):
+ *   pX = pY = (1 - e^{-t/T1}) / 4,  pZ = (1 - e^{-t/T2}) / 2 - (1 - e^{-t/T1}) / 4.
+ * out: (pX, pY, pZ).  TUSQ_ERR_INVALID_ARG if t < 0, T1 <= 0, T2 <= 0 or pZ < 0 (T2 > 2 T1 is
+ * unphysical). */
+tusq_status tusq_twirl_decoherence(double t, double T1, double T2, double out[3]);
 
 /* Pruning (reading #10): significant iff count*alpha_den >= alpha_num*p0;
  * beta >= 1 insignificant leaves kept count-proportionally.  NULL -> 1/100, 100, enabled. */

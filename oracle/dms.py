@@ -109,3 +109,27 @@ def dms_run(n: int, ops, p1: float, p2: float, pm: float) -> np.ndarray:
         for q in range(n):
             rho = channel(rho, n, q, (1 - pm, pm, 0, 0))
     return np.real(np.diag(rho)).copy()
+
+
+def dms_run_chan(n: int, ops, chan1, chan2, chanm) -> np.ndarray:
+    """Exact noisy output distribution for general Pauli channels (Eq. 2): chan1 =
+    (pX, pY, pZ) after every 1q gate, chan2 on each qubit of every 2q gate, chanm before readout."""
+    N = 1 << n
+    rho = np.zeros((N, N), dtype=complex)
+    rho[0, 0] = 1
+
+    def probs(c):
+        return (1 - sum(c), c[0], c[1], c[2])
+    for g in ops:
+        U = full_gate(n, g)
+        rho = U @ rho @ U.conj().T
+        if g[0] in (13, 14, 15):
+            if any(chan2):
+                for q in (g[1], g[2]):
+                    rho = channel(rho, n, q, probs(chan2))
+        elif any(chan1):
+            rho = channel(rho, n, g[1], probs(chan1))
+    if any(chanm):
+        for q in range(n):
+            rho = channel(rho, n, q, probs(chanm))
+    return np.real(np.diag(rho)).copy()

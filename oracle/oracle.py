@@ -54,6 +54,11 @@ def lib():
         L.or_build.argtypes = [C.c_uint32, C.c_void_p, C.c_uint64, C.c_double, C.c_double, C.c_double,
                                C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
                                C.POINTER(C.c_void_p)]
+        L.or_build_chan.argtypes = [C.c_uint32, C.c_void_p, C.c_uint64, dp, C.c_uint64, C.c_uint64, C.c_uint32,
+                                    C.c_uint32, C.c_uint32, C.c_int, C.POINTER(C.c_void_p)]
+        L.or_site_table_chan.restype = C.c_uint64
+        L.or_site_table_chan.argtypes = [C.c_uint32, C.c_void_p, C.c_uint64, dp, C.c_void_p]
+        L.or_twirl.argtypes = [C.c_double, C.c_double, C.c_double, dp]
         L.or_free.argtypes = [C.c_void_p]
         L.or_stats.argtypes = [C.c_void_p, u64p]
         L.or_leaf.restype = C.c_uint32
@@ -101,6 +106,29 @@ def site_table(n, ops, p1, p2, pm) -> np.ndarray:
     out = np.zeros(max(m, 1), dtype=SITE_DTYPE)
     lib().or_site_table(n, a.ctypes.data, len(ops), p1, p2, pm, out.ctypes.data)
     return out[:m]
+
+
+def _chan_array(chan) -> np.ndarray:
+    c = np.array([x for t in chan for x in t], dtype=np.float64)
+    assert c.shape == (9,)
+    return c
+
+
+def site_table_chan(n, ops, chan) -> np.ndarray:
+    """Sites for general Pauli channels chan = ((pX,pY,pZ) 1q, (..) 2q, (..) readout)."""
+    a = ops_array(ops)
+    c = _chan_array(chan)
+    m = lib().or_site_table_chan(n, a.ctypes.data, len(ops), _ptr(c, C.c_double), None)
+    out = np.zeros(max(m, 1), dtype=SITE_DTYPE)
+    lib().or_site_table_chan(n, a.ctypes.data, len(ops), _ptr(c, C.c_double), out.ctypes.data)
+    return out[:m]
+
+
+def twirl(t: float, T1: float, T2: float):
+    """Eq. 2: Pauli-twirled decoherence (pX, pY, pZ), or None when unphysical / invalid."""
+    o = np.zeros(3)
+    rc = lib().or_twirl(t, T1, T2, _ptr(o, C.c_double))
+    return None if rc else tuple(float(x) for x in o)
 
 
 def sample_er(n, ops, p1, p2, pm, seed, shot) -> List[Tuple[int, int]]:
@@ -172,12 +200,19 @@ class Tree:
 
     STAT_NAMES = ["S1", "S2", "S3", "p0", "n_sig", "n_insig", "n_selected", "n_leaves", "n_ops"]
 
-    def __init__(self, n, ops, p1, p2, pm, shots, seed, alpha=(1, 100), beta=100, prune=True):
+    def __init__(self, n, ops, p1, p2, pm, shots, seed, alpha=(1, 100), beta=100, prune=True, chan=None):
+        """chan: None (depolarizing p1/p2 + readout bit flip pm) or three (pX, pY, pZ) triples for
+        the 1q-gate, 2q-gate and readout sites (Eq. 2)."""
         self.n, self.ops, self.seed = n, list(ops), seed
         self._ops = ops_array(ops)
         h = C.c_void_p()
-        rc = lib().or_build(n, self._ops.ctypes.data, len(ops), p1, p2, pm, shots, seed, alpha[0], alpha[1],
-                            beta, int(prune), C.byref(h))
+        if chan is not None:
+            c = _chan_array(chan)
+            rc = lib().or_build_chan(n, self._ops.ctypes.data, len(ops), _ptr(c, C.c_double), shots, seed,
+                                     alpha[0], alpha[1], beta, int(prune), C.byref(h))
+        else:
+            rc = lib().or_build(n, self._ops.ctypes.data, len(ops), p1, p2, pm, shots, seed, alpha[0], alpha[1],
+                                beta, int(prune), C.byref(h))
         if rc != 0:
             raise ValueError(f"or_build failed rc={rc}")
         self.h = h
@@ -185,7 +220,8 @@ class Tree:
     @classmethod
     def from_config(cls, cfg, prune=True):
         nz = cfg.noise
-        return cls(cfg.n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed, cfg.alpha, cfg.beta, prune)
+        return cls(cfg.n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed, cfg.alpha, cfg.beta, prune,
+                   chan=getattr(nz, "pauli", None))
 
     def __del__(self):
         if getattr(self, "h", None):

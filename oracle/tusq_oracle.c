@@ -82,18 +82,25 @@ typedef struct { uint32_t pos, q; uint64_t tI, tX, tY, tZ; } or_site;
 
 static uint64_t thr(double p) { return (uint64_t)llround(p * 4294967296.0); }
 
-static void set_depolarizing(or_site *s, double p)
+/* A site's Pauli channel (pX, pY, pZ) as integer thresholds (reading #9): t_P = round(p_P 2^32),
+ * t_I = 2^32 - (t_X + t_Y + t_Z); a channel summing to 1 may round past 2^32 -- the excess comes
+ * off t_Y, then t_Z. */
+static void set_channel(or_site *s, const double c[3])
 {
-    double third = p / 3.0;
-    s->tX = thr(third); s->tY = thr(third); s->tZ = thr(third);
-    s->tI = 4294967296ull - (s->tX + s->tY + s->tZ);
+    const uint64_t one = 4294967296ull;
+    s->tX = thr(c[0]); if (s->tX > one) s->tX = one;
+    s->tY = thr(c[1]);
+    s->tZ = thr(c[2]);
+    if (s->tX + s->tY > one) s->tY = one - s->tX;
+    if (s->tX + s->tY + s->tZ > one) s->tZ = one - s->tX - s->tY;
+    s->tI = one - (s->tX + s->tY + s->tZ);
 }
 
-static void set_bitflip(or_site *s, double p)
-{
-    s->tX = thr(p); s->tY = 0; s->tZ = 0;
-    s->tI = 4294967296ull - s->tX;
-}
+/* depolarizing p (reading #2) -> (p/3, p/3, p/3); measurement bit flip p (P:137,
+ * reading #4) -> (p, 0, 0) */
+static void chan_depolarizing(double p, double c[3]) { c[0] = c[1] = c[2] = p / 3.0; }
+static void chan_bitflip(double p, double c[3]) { c[0] = p; c[1] = 0.0; c[2] = 0.0; }
+static int chan_live(const double c[3]) { return c[0] > 0.0 || c[1] > 0.0 || c[2] > 0.0; }
 
 int or_validate(uint32_t n, const or_op *ops, uint64_t L)
 {
@@ -106,30 +113,47 @@ int or_validate(uint32_t n, const or_op *ops, uint64_t L)
     return 0;
 }
 
-/* Returns the number of sites; fills `out` when non-NULL. */
-uint64_t or_site_table(uint32_t n, const or_op *ops, uint64_t L, double p1, double p2, double pm, or_site *out)
+/* Sites for general per-class Pauli channels chan[0..2] (1q gates), chan[3..5] (each qubit of a 2q
+ * gate), chan[6..8] (readout); a class whose channel is all-zero attaches no site (reading #21).
+ * Returns the number of sites; fills `out` when non-NULL. */
+uint64_t or_site_table_chan(uint32_t n, const or_op *ops, uint64_t L, const double chan[9], or_site *out)
 {
     uint64_t m = 0;
     for (uint64_t pos = 0; pos < L; pos++) {
         if (is_two_qubit(ops[pos].kind)) {
-            if (p2 > 0.0) {
-                if (out) { out[m].pos = (uint32_t)pos; out[m].q = ops[pos].q0; set_depolarizing(&out[m], p2); }
+            if (chan_live(chan + 3)) {
+                if (out) { out[m].pos = (uint32_t)pos; out[m].q = ops[pos].q0; set_channel(&out[m], chan + 3); }
                 m++;
-                if (out) { out[m].pos = (uint32_t)pos; out[m].q = ops[pos].q1; set_depolarizing(&out[m], p2); }
+                if (out) { out[m].pos = (uint32_t)pos; out[m].q = ops[pos].q1; set_channel(&out[m], chan + 3); }
                 m++;
             }
-        } else if (p1 > 0.0) {
-            if (out) { out[m].pos = (uint32_t)pos; out[m].q = ops[pos].q0; set_depolarizing(&out[m], p1); }
+        } else if (chan_live(chan)) {
+            if (out) { out[m].pos = (uint32_t)pos; out[m].q = ops[pos].q0; set_channel(&out[m], chan); }
             m++;
         }
     }
-    if (pm > 0.0) {
+    if (chan_live(chan + 6)) {
         for (uint32_t q = 0; q < n; q++) {
-            if (out) { out[m].pos = (uint32_t)L; out[m].q = q; set_bitflip(&out[m], pm); }
+            if (out) { out[m].pos = (uint32_t)L; out[m].q = q; set_channel(&out[m], chan + 6); }
             m++;
         }
     }
     return m;
+}
+
+static void chan_of(double p1, double p2, double pm, double chan[9])
+{
+    chan_depolarizing(p1, chan);
+    chan_depolarizing(p2, chan + 3);
+    chan_bitflip(pm, chan + 6);
+}
+
+/* depolarizing p1 / p2 + readout bit flip pm */
+uint64_t or_site_table(uint32_t n, const or_op *ops, uint64_t L, double p1, double p2, double pm, or_site *out)
+{
+    double chan[9];
+    chan_of(p1, p2, pm, chan);
+    return or_site_table_chan(n, ops, L, chan, out);
 }
 
 /* ===================================================================== ER sampling
@@ -482,17 +506,22 @@ static void free_recs(or_leafrec *r, uint64_t m)
     free(r);
 }
 
-int or_build(uint32_t n, const or_op *ops, uint64_t L, double p1, double p2, double pm,
-             uint64_t shots, uint64_t seed, uint32_t a_num, uint32_t a_den, uint32_t beta,
-             int prune_enabled, void **out)
+int or_build_chan(uint32_t n, const or_op *ops, uint64_t L, const double chan[9],
+                  uint64_t shots, uint64_t seed, uint32_t a_num, uint32_t a_den, uint32_t beta,
+                  int prune_enabled, void **out)
 {
     *out = NULL;
     if (or_validate(n, ops, L) || shots == 0 || a_den == 0) return 1;
     if (prune_enabled && (beta == 0 || a_num > a_den)) return 1;   /* beta >= 1 keeps shots conserved */
-    if (!(p1 >= 0 && p1 <= 1) || !(p2 >= 0 && p2 <= 1) || !(pm >= 0 && pm <= 1)) return 1;
-    uint64_t m = or_site_table(n, ops, L, p1, p2, pm, NULL);
+    for (int c = 0; c < 3; c++) {
+        const double *p = chan + 3 * c;
+        if (!(p[0] >= 0 && p[0] <= 1) || !(p[1] >= 0 && p[1] <= 1) || !(p[2] >= 0 && p[2] <= 1) ||
+            !(p[0] + p[1] + p[2] <= 1))
+            return 1;
+    }
+    uint64_t m = or_site_table_chan(n, ops, L, chan, NULL);
     or_site *sites = (or_site *)malloc((m ? m : 1) * sizeof(or_site));
-    or_site_table(n, ops, L, p1, p2, pm, sites);
+    or_site_table_chan(n, ops, L, chan, sites);
 
     /* S1 raw ERs, one per shot */
     or_leafrec *raw = (or_leafrec *)calloc(shots, sizeof(or_leafrec));
@@ -579,6 +608,28 @@ int or_build(uint32_t n, const or_op *ops, uint64_t L, double p1, double p2, dou
     t->n_leaves = nl;
     free(can); free(cin); free(cout); free(cls);
     *out = t;
+    return 0;
+}
+
+int or_build(uint32_t n, const or_op *ops, uint64_t L, double p1, double p2, double pm,
+             uint64_t shots, uint64_t seed, uint32_t a_num, uint32_t a_den, uint32_t beta,
+             int prune_enabled, void **out)
+{
+    double chan[9];
+    *out = NULL;
+    if (!(p1 >= 0 && p1 <= 1) || !(p2 >= 0 && p2 <= 1) || !(pm >= 0 && pm <= 1)) return 1;
+    chan_of(p1, p2, pm, chan);
+    return or_build_chan(n, ops, L, chan, shots, seed, a_num, a_den, beta, prune_enabled, out);
+}
+
+/* Eq. 2: Pauli twirl of decoherence for an idle time t -> (pX, pY, pZ); 1 on bad input */
+int or_twirl(double t, double T1, double T2, double out[3])
+{
+    if (!(t >= 0) || !(T1 > 0) || !(T2 > 0)) return 1;
+    double px = (1.0 - exp(-t / T1)) / 4.0;
+    double pz = (1.0 - exp(-t / T2)) / 2.0 - (1.0 - exp(-t / T1)) / 4.0;
+    if (pz < 0) return 1;
+    out[0] = px; out[1] = px; out[2] = pz;
     return 0;
 }
 

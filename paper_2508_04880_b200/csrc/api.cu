@@ -3,6 +3,7 @@
 // tile sweeps (K5) or per-gate kernels (K1-K4), leaf sampling (K6) into shot slots.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -85,7 +86,14 @@ tusq_status tusq_build_error_tree(uint32_t n, const tusq_op *ops, uint64_t L, co
     if (s) return s;
     if (!noise) return fail(TUSQ_ERR_INVALID_ARG, "noise is NULL");
     auto okp = [](double p) { return p >= 0.0 && p <= 1.0; };
-    if (!okp(noise->p1) || !okp(noise->p2) || !okp(noise->p_meas)) return fail(TUSQ_ERR_INVALID_ARG, "p outside [0, 1]");
+    if (noise->flags & ~TUSQ_NOISE_PAULI) return fail(TUSQ_ERR_INVALID_ARG, "unknown noise flags");
+    if (noise->flags & TUSQ_NOISE_PAULI) {
+        for (const double *c : {noise->pauli1, noise->pauli2, noise->pauli_meas})
+            if (!okp(c[0]) || !okp(c[1]) || !okp(c[2]) || !(c[0] + c[1] + c[2] <= 1.0))
+                return fail(TUSQ_ERR_INVALID_ARG, "Pauli channel probabilities outside [0, 1] or summing above 1");
+    } else if (!okp(noise->p1) || !okp(noise->p2) || !okp(noise->p_meas)) {
+        return fail(TUSQ_ERR_INVALID_ARG, "p outside [0, 1]");
+    }
     if (shots == 0) return fail(TUSQ_ERR_INVALID_ARG, "shots must be > 0");
     tusq_prune pr = prune ? *prune : tusq_prune{1, 100, 100, 1};
     if (pr.enabled && (pr.alpha_den == 0 || pr.alpha_num > pr.alpha_den))
@@ -98,6 +106,20 @@ tusq_status tusq_build_error_tree(uint32_t n, const tusq_op *ops, uint64_t L, co
     } catch (...) {
         return fail(TUSQ_ERR_INTERNAL, "exception in tusq_build_error_tree");
     }
+}
+
+tusq_status tusq_twirl_decoherence(double t, double T1, double T2, double out[3])
+{
+    if (!out) return fail(TUSQ_ERR_INVALID_ARG, "out is NULL");
+    if (!(t >= 0.0) || !(T1 > 0.0) || !(T2 > 0.0)) return fail(TUSQ_ERR_INVALID_ARG, "need t >= 0, T1 > 0, T2 > 0");
+    // Eq. 2: Pauli-twirled amplitude and phase damping
+    const double a = (1.0 - std::exp(-t / T1)) / 4.0;
+    const double z = (1.0 - std::exp(-t / T2)) / 2.0 - a;
+    if (z < 0.0) return fail(TUSQ_ERR_INVALID_ARG, "unphysical decoherence: p_Z < 0 (T2 > 2 T1)");
+    out[0] = a;
+    out[1] = a;
+    out[2] = z;
+    return TUSQ_OK;
 }
 
 tusq_status tusq_tree_get_info(const tusq_tree *t, tusq_tree_info *out)

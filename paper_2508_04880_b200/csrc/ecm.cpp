@@ -25,25 +25,48 @@ struct Site {
 
 uint64_t round_u32(double p) { return (uint64_t)std::llround(p * 4294967296.0); }
 
+// The (pX, pY, pZ) channel of each site class: depolarizing p -> (p/3, p/3, p/3), bit flip p ->
+// (p, 0, 0) (readings #2, #4), or the caller's general Pauli channels (TUSQ_NOISE_PAULI, Eq. 2).
+struct Chan { double x, y, z; };
+
+static void channels(const tusq_noise &nz, Chan &c1, Chan &c2, Chan &cm)
+{
+    if (nz.flags & TUSQ_NOISE_PAULI) {
+        c1 = Chan{nz.pauli1[0], nz.pauli1[1], nz.pauli1[2]};
+        c2 = Chan{nz.pauli2[0], nz.pauli2[1], nz.pauli2[2]};
+        cm = Chan{nz.pauli_meas[0], nz.pauli_meas[1], nz.pauli_meas[2]};
+    } else {
+        c1 = Chan{nz.p1 / 3.0, nz.p1 / 3.0, nz.p1 / 3.0};
+        c2 = Chan{nz.p2 / 3.0, nz.p2 / 3.0, nz.p2 / 3.0};
+        cm = Chan{nz.p_meas, 0.0, 0.0};
+    }
+}
+
 std::vector<Site> make_sites(uint32_t n, const std::vector<Op> &g, const tusq_noise &nz)
 {
     std::vector<Site> s;
-    auto dep = [&](uint32_t pos, uint32_t q, double p) {
-        uint64_t t = round_u32(p / 3.0);
-        uint64_t tI = 4294967296ull - 3 * t;
-        s.push_back(Site{pos, q, tI, tI + t, tI + 2 * t});
+    Chan c1, c2, cm;
+    channels(nz, c1, c2, cm);
+    auto live = [](const Chan &c) { return c.x > 0 || c.y > 0 || c.z > 0; };   // reading #21
+    auto add = [&](uint32_t pos, uint32_t q, const Chan &c) {
+        const uint64_t one = 4294967296ull;
+        uint64_t tX = std::min(round_u32(c.x), one), tY = round_u32(c.y), tZ = round_u32(c.z);
+        // rounding may push a channel that sums to 1 past 2^32: the excess comes off Y, then Z
+        // (reading #9); tI = 0 then
+        if (tX + tY > one) tY = one - tX;
+        if (tX + tY + tZ > one) tZ = one - tX - tY;
+        const uint64_t tI = one - (tX + tY + tZ);
+        s.push_back(Site{pos, q, tI, tI + tX, tI + tX + tY});
     };
     for (uint32_t pos = 0; pos < g.size(); ++pos) {
         if (two_qubit(g[pos].kind)) {
-            if (nz.p2 > 0) { dep(pos, g[pos].q0, nz.p2); dep(pos, g[pos].q1, nz.p2); }
-        } else if (nz.p1 > 0) {
-            dep(pos, g[pos].q0, nz.p1);
+            if (live(c2)) { add(pos, g[pos].q0, c2); add(pos, g[pos].q1, c2); }
+        } else if (live(c1)) {
+            add(pos, g[pos].q0, c1);
         }
     }
-    if (nz.p_meas > 0) {
-        uint64_t t = round_u32(nz.p_meas), tI = 4294967296ull - t;
-        for (uint32_t q = 0; q < n; ++q) s.push_back(Site{(uint32_t)g.size(), q, tI, tI + t, tI + t});
-    }
+    if (live(cm))
+        for (uint32_t q = 0; q < n; ++q) add((uint32_t)g.size(), q, cm);
     return s;
 }
 

@@ -27,7 +27,11 @@ OP_DTYPE = np.dtype([("kind", "<u4"), ("q0", "<u4"), ("q1", "<u4"), ("_pad", "<u
 
 class Noise(C.Structure):
     _fields_ = [("p1", C.c_double), ("p2", C.c_double), ("p_meas", C.c_double), ("flags", C.c_uint32),
-                ("_pad", C.c_uint32)]
+                ("_pad", C.c_uint32), ("pauli1", C.c_double * 3), ("pauli2", C.c_double * 3),
+                ("pauli_meas", C.c_double * 3)]
+
+
+NOISE_PAULI = 0x1
 
 
 class Prune(C.Structure):
@@ -77,6 +81,7 @@ _sigs = {
     "tusq_comm_init": [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
     "tusq_comm_init_local": [C.c_int, C.c_int, C.POINTER(_vp)],
     "tusq_reduce_slots": [_vp, _u64p, C.c_uint64, _vp],
+    "tusq_twirl_decoherence": [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)],
 }
 for _name, _args in _sigs.items():
     getattr(_lib, _name).argtypes = _args
@@ -173,10 +178,17 @@ class Tree:
 
 
 def build_error_tree(n: int, ops, p1: float, p2: float, p_meas: float, shots: int, seed: int,
-                     alpha=(1, 100), beta: int = 100, prune: bool = True) -> Tree:
+                     alpha=(1, 100), beta: int = 100, prune: bool = True, pauli=None) -> Tree:
+    """pauli: None (depolarizing p1/p2 + bit flip p_meas) or three (pX, pY, pZ) triples for the
+    1q-gate, 2q-gate and readout sites (TUSQ_NOISE_PAULI; p1/p2/p_meas are then ignored)."""
     a = pack_ops(ops)
     h = C.c_void_p()
     nz = Noise(p1, p2, p_meas, 0, 0)
+    if pauli is not None:
+        nz.flags = NOISE_PAULI
+        for dst, src in zip((nz.pauli1, nz.pauli2, nz.pauli_meas), pauli):
+            for i in range(3):
+                dst[i] = float(src[i])
     pr = Prune(alpha[0], alpha[1], beta, 1 if prune else 0)
     _check(_lib.tusq_build_error_tree(n, a.ctypes.data, len(ops), C.byref(nz), shots, seed, C.byref(pr), C.byref(h)),
            "tusq_build_error_tree")
@@ -266,3 +278,10 @@ def reduce_slots(comm: "Comm", slots: np.ndarray, stream=None) -> np.ndarray:
         raise ValueError("slots must be a C-contiguous uint64 array")
     _check(_lib.tusq_reduce_slots(comm.h, slots.ctypes.data_as(_u64p), slots.size, _ptr(stream)), "tusq_reduce_slots")
     return slots
+
+
+def twirl_decoherence(t: float, T1: float, T2: float):
+    """(pX, pY, pZ) of the Pauli-twirled decoherence channel (Eq. 2) -- tusq_twirl_decoherence."""
+    out = (C.c_double * 3)()
+    _check(_lib.tusq_twirl_decoherence(t, T1, T2, out), "tusq_twirl_decoherence")
+    return tuple(out)

@@ -361,3 +361,29 @@ def test_run_tree_errors(T, torch):
     assert e.value.status == 2
     with pytest.raises(ValueError):
         T.run_tree(t, 128, out_slots=np.zeros(10, dtype=np.uint64))
+
+
+# ------------------------------------------------------------------ general Pauli channels (Eq. 2)
+def test_qaoa_twirled_decoherence_slots(T, torch, oracle_runs):
+    # Q13: the paper's QAOA at 13 qubits under Pauli-twirled decoherence on
+    # every gate and a readout channel -- ECM -> DFTT -> sampling, slot for slot vs the oracle
+    cfg = W.config("Q13")
+    t = T.build_error_tree(cfg.n, cfg.ops, 0, 0, 0, cfg.shots, cfg.seed, pauli=cfg.noise.pauli)
+    ref, edge = oracle_runs.run("Q13")
+    for flags in (0, T.EXEC_NO_FUSE):
+        slots, stats = T.run_tree(t, 128, flags=flags)
+        _check_slots(slots, ref, edge, cfg.shots)
+        assert stats["draws"] == cfg.shots
+
+
+def test_random_asymmetric_channels_slots(T, torch, oracle):
+    rng = np.random.default_rng(91)
+    for trial in range(6):
+        n = int(rng.integers(3, 15))
+        ops = W.random_circuit(rng, n, int(rng.integers(20, 80)))
+        chan = [tuple(float(x) for x in rng.dirichlet([1, 1, 1, 1])[:3] * 0.05) for _ in range(3)]
+        t = T.build_error_tree(n, ops, 0, 0, 0, 2048, 100 + trial, pauli=chan)
+        ot = oracle.Tree(n, ops, 0, 0, 0, 2048, 100 + trial, chan=chan)
+        ref, edge = ot.run()
+        slots, _ = T.run_tree(t, 128)
+        _check_slots(slots, ref, edge, 2048)

@@ -524,3 +524,63 @@ def test_sparse_sampler_matches_dense_sampler(oracle):
         got, gedge = SP.sample(sp, seed, leaf, nd, 1e-3)
         assert np.array_equal(np.array(got, dtype=np.uint64), ref), trial
         assert np.array_equal(np.array(gedge), redge), trial
+
+
+# ------------------------------------------------------------------ general Pauli channels (Eq. 2)
+def test_twirl_closed_forms(oracle):
+    # pX = pY = (1 - e^{-t/T1})/4, pZ = (1 - e^{-t/T2})/2 - (1 - e^{-t/T1})/4
+    c = (1 - math.exp(-1)) / 4                      # t = T1 = T2: all three equal, ~0.158
+    assert np.allclose(oracle.twirl(1.0, 1.0, 1.0), (c, c, c), atol=1e-15, rtol=0) and abs(c - 0.158) < 1e-3
+    px, py, pz = oracle.twirl(3.0, 3.0, 6.0)        # T2 = 2 T1, t = T1
+    assert px == py and abs(pz - ((1 - math.exp(-0.5)) / 2 - (1 - math.exp(-1)) / 4)) < 1e-15
+    assert oracle.twirl(0.0, 1.0, 1.0) == (0.0, 0.0, 0.0)
+    assert oracle.twirl(1.0, 1.0, 3.0) is None      # T2 > 2 T1: p_Z < 0, unphysical
+    assert W.TWIRL_NOISE.pauli[0] == oracle.twirl(0.02, 1.0, 1.0)   # the Q13 config's numbers
+
+
+def _enumerate_exact_chan(oracle, n, ops, chan, canonical):
+    sites = oracle.site_table_chan(n, ops, chan)
+    choices = []
+    for s in sites:
+        pos = int(s["pos"])
+        c = chan[2] if pos == len(ops) else (chan[1] if ops[pos][0] in W.TWO_QUBIT else chan[0])
+        choices.append([(p, w) for p, w in ((PI, 1 - sum(c)), (PX, c[0]), (PY, c[1]), (PZ, c[2])) if w > 0])
+    P = np.zeros(1 << n)
+    for combo in itertools.product(*choices):
+        w = np.prod([c[1] for c in combo])
+        ins = [(int(s["pos"]), int(s["q"]), c[0]) for s, c in zip(sites, combo) if c[0] != PI]
+        if canonical:
+            st = oracle.replay(n, ops, oracle.canonicalize(n, ops, ins), before_gate=True)
+        else:
+            st = oracle.replay(n, ops, ins, before_gate=False)
+        P += w * np.abs(st) ** 2
+    return P
+
+
+def test_brute_force_general_channel_matches_dms(oracle):
+    # P:139-147 + SPEC S:405 with NON-depolarizing channels (asymmetric pX/pY/pZ, a readout channel
+    # with Y and Z parts): sum over all ERs of Pr(ER)|psi_ER|^2 == diag(rho), for the raw and the
+    # canonical (commuted) Pauli placement; then the sampling pipeline converges to it
+    n = 2
+    ops = [W.op(W.H, 0), W.op(W.T, 0), W.op(W.H, 0), W.op(W.CX, 0, 1), W.op(W.RZ, 1, 0, 0.7), W.op(W.H, 1)]
+    chan = ((0.05, 0.01, 0.08), (0.02, 0.09, 0.03), (0.06, 0.02, 0.04))
+    ref = dms.dms_run_chan(n, ops, *chan)
+    assert abs(ref.sum() - 1) < 1e-12
+    for canonical in (False, True):
+        P = _enumerate_exact_chan(oracle, n, ops, chan, canonical)
+        assert np.abs(P - ref).max() < 1e-12
+    t = oracle.Tree(n, ops, 0, 0, 0, 200000, 77, prune=False, chan=chan)
+    slots, _ = t.run()
+    hist = np.bincount(slots.astype(np.int64), minlength=1 << n) / len(slots)
+    assert 0.5 * np.abs(hist - ref).sum() <= 0.01
+
+
+def test_depolarizing_is_the_symmetric_pauli_channel(oracle):
+    # the depolarizing site table (p/3, p/3, p/3) and bit flip (p, 0, 0) equal the general form
+    n, ops = W.qft(4)
+    a = oracle.site_table(n, ops, 0.01, 0.02, 0.03)
+    b = oracle.site_table_chan(n, ops, ((0.01 / 3,) * 3, (0.02 / 3,) * 3, (0.03, 0.0, 0.0)))
+    assert np.array_equal(a, b)
+    t1 = oracle.Tree(n, ops, 0.01, 0.02, 0.03, 4096, 5)
+    t2 = oracle.Tree(n, ops, 0, 0, 0, 4096, 5, chan=((0.01 / 3,) * 3, (0.02 / 3,) * 3, (0.03, 0.0, 0.0)))
+    assert t1.serialize() == t2.serialize()

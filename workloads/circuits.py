@@ -138,12 +138,53 @@ def qft(n: int, native_cp: bool = False) -> Tuple[int, List[Op]]:
     return n, ops
 
 
+# ---------------------------------------------------------------- QAOA
+def qaoa(n: int, layers: int, seed: int = 1) -> Tuple[int, List[Op]]:
+    """Supermarq-style QAOA block: H on every qubit, then per layer one parameterized
+    single-qubit layer on all qubits (RX, then RZ) followed by CNOT entanglers (a linear chain).
+    Angles are uniform in [0, 2 pi) from a seeded generator (the paper gives none)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    ops: List[Op] = [op(H, q) for q in range(n)]
+    for _ in range(layers):
+        th = rng.uniform(0, 2 * math.pi, size=n)
+        ph = rng.uniform(0, 2 * math.pi, size=n)
+        ops += [op(RX, q, 0, float(th[q])) for q in range(n)]
+        ops += [op(RZ, q, 0, float(ph[q])) for q in range(n)]
+        ops += [op(CX, q, q + 1) for q in range(n - 1)]
+    return n, ops
+
+
+# ---------------------------------------------------------------- Bernstein-Vazirani (P:509)
+def bv_secret(n: int) -> int:
+    return 0x2D2D2D2D2D2D2D2D & ((1 << (n - 1)) - 1)
+
+
+def bv(n: int) -> Tuple[int, List[Op]]:
+    """Bernstein-Vazirani on n-1 data qubits + ancilla n-1 (the delta study of P:509-516): X and H on
+    the ancilla, H on the data, CX(i -> ancilla) for each secret bit, H on every qubit.  Noiseless
+    output: the secret on the data qubits and 1 on the ancilla (bv_expected_output)."""
+    s = bv_secret(n)
+    a = n - 1
+    ops: List[Op] = [op(X, a)] + [op(H, q) for q in range(n)]
+    ops += [op(CX, q, a) for q in range(n - 1) if (s >> q) & 1]
+    ops += [op(H, q) for q in range(n)]
+    return n, ops
+
+
+def bv_expected_output(n: int) -> int:
+    return bv_secret(n) | (1 << (n - 1))
+
+
 # ---------------------------------------------------------------- configs (SURVEY 8(d))
 @dataclass
 class Noise:
     p1: float = 1e-3      # depolarizing after every 1q gate (paper convention 1-p, p/3 x3)
     p2: float = 1e-2      # depolarizing on each qubit of a 2q gate (reading #1)
     p_meas: float = 0.0   # bit flip before readout on every qubit (reading #4)
+    # general Pauli channels (Eq. 2): ((pX,pY,pZ) 1q gates, (..) 2q-gate qubits, (..) readout);
+    # when set, p1/p2/p_meas are ignored
+    pauli: tuple = None
 
 
 @dataclass
@@ -182,7 +223,18 @@ def config(name: str, seed: int = 1) -> Config:
     if name == "C5":
         n, ops = qft(34, native_cp=True)
         return Config("C5", n, ops, MEAS_NOISE, 8192, seed)
+    if name == "Q13":   # P:455 QAOA at its smallest size with twirled decoherence (Eq. 2) -- SURVEY 8(f)#4
+        n, ops = qaoa(13, 2, seed)
+        return Config("Q13", n, ops, TWIRL_NOISE, 8192, seed)
     raise KeyError(name)
+
+
+# Eq. 2 twirled decoherence for an idle time t = T1 / 50, T2 = T1 (pX = pY = pZ =
+# (1 - e^{-0.02}) / 4 each), composed by the caller into the 1q/2q/readout channels; the numbers
+# are inputs here -- tusq_twirl_decoherence / the oracle's or_twirl compute the same map
+TWIRL_NOISE = Noise(pauli=((0.004950331673311187, 0.004950331673311187, 0.004950331673311187),
+                           (0.004950331673311187, 0.004950331673311187, 0.004950331673311187),
+                           (0.01, 0.0, 0.0)))
 
 
 def random_circuit(rng, n: int, n_gates: int, kinds=None) -> List[Op]:
