@@ -124,7 +124,11 @@ typedef struct {
 #define TUSQ_EXEC_PLAN_ONLY   0x10u /* run the scheduler and planner only: fill stats, launch nothing */
 #define TUSQ_EXEC_PROFILE     0x20u /* bracket every gate-kernel launch with CUDA events (stats.gate_kernel_*) */
 #define TUSQ_EXEC_CONTINUE    0x40u /* d_state already holds the final state of leaf leaf_begin-1 (left by a
-                                       previous call): continue the DFS from there instead of re-anchoring */
+                                       previous call): continue the DFS from there instead of re-anchoring
+                                       (a hint: the small-n batched path re-anchors every sub-range) */
+#define TUSQ_EXEC_NO_BATCH    0x80u /* n <= 13 (c128) / 14 (c64): do not run the batched on-chip path (one
+                                       launch, one DFS sub-range per CTA, state in shared memory) but one
+                                       transition at a time like larger n */
 
 /* exec.mode */
 #define TUSQ_MODE_REPLICA 0u    /* the whole 2^n vector on this device (leaf ranges shard across replicas) */

@@ -247,16 +247,27 @@ tusq_status tusq_apply_ops(void *d_state, uint32_t n, uint32_t precision, const 
     ctx.psi = d_state; ctx.n = n; ctx.prec = (int)precision; ctx.st = (cudaStream_t)stream; ctx.stats = &stats;
     ctx.dry = (flags & TUSQ_APPLY_PLAN_ONLY) != 0;
     FusedPlanner planner(n, (int)precision);
+    void *alt = nullptr;
+    const bool fused = !(flags & TUSQ_APPLY_UNFUSED) && planner.enabled();
+    if (fused && !ctx.dry && L > 0) {   // second buffer for the layout-changing sweeps (optional)
+        if (cudaMallocAsync(&alt, (precision == 128 ? 16ull : 8ull) << n, ctx.st) != cudaSuccess) {
+            cudaGetLastError();
+            alt = nullptr;
+        }
+        planner.set_alt(alt);
+    }
     try {
-        if (!(flags & TUSQ_APPLY_UNFUSED) && planner.enabled()) {
+        if (fused) {
             planner.execute(v, ctx);
             planner.materialize(ctx);
         } else {
             execute_unfused(v, ctx);
         }
     } catch (const std::exception &e) {
+        if (alt) cudaFreeAsync(alt, ctx.st);
         return fail(TUSQ_ERR_INTERNAL, e.what());
     }
+    if (alt) cudaFreeAsync(alt, ctx.st);
     if (!ctx.dry) TQ_CUDA(cudaGetLastError());
     return TUSQ_OK;
 }
@@ -382,9 +393,12 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     uint32_t *d_edges = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     GateTimer timer(!dry && (ex->flags & TUSQ_EXEC_PROFILE));
+    void *alt_buf = nullptr;   // set below, freed here
     auto cleanup = [&]() {
         if (scr) cudaFreeAsync(scr, st);
-        if (own_state) { cudaStreamSynchronize(st); cudaFree(psi); }
+        if (own_state || alt_buf) cudaStreamSynchronize(st);
+        if (own_state) cudaFree(psi);
+        if (alt_buf) cudaFree(alt_buf);
         for (auto &e : ev) if (e) cudaEventDestroy(e);
     };
 #define TQ_RUN_CUDA(call)                                                                            \
@@ -412,6 +426,16 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     const double eps = ex->edge_eps > 0 ? ex->edge_eps : (prec == 128 ? 1e-9 : 1e-5);
     FusedPlanner planner(n, prec);
     const bool fuse = !(ex->flags & TUSQ_EXEC_NO_FUSE) && planner.enabled();
+    // small n: the whole range in ONE launch, one sub-range per CTA, state on chip (smallsim.cu)
+    const bool small = !(ex->flags & (TUSQ_EXEC_NO_FUSE | TUSQ_EXEC_NO_BATCH)) && n <= small_max_qubits(prec);
+    // the fused path's second buffer (layout-changing sweeps run out of place); without the memory
+    // for it every sweep keeps the identity layout and runs in place
+    void *alt = nullptr;
+    if (fuse && !small && !dry && le > lb) {
+        if (cudaMalloc(&alt, need) != cudaSuccess) { cudaGetLastError(); alt = nullptr; }
+        planner.set_alt(alt);
+        alt_buf = alt;
+    }
     Ctx ctx;
     ctx.psi = psi; ctx.n = n; ctx.prec = prec; ctx.st = st; ctx.dry = dry; ctx.stats = &stats;
     ctx.timer = timer.on() ? &timer : nullptr;
@@ -420,6 +444,11 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     uint64_t since_anchor = 0;
     bool phys_sums_valid = false;
     try {
+        if (small) {
+            tusq_status ss = run_tree_small(t, ex, lb, le, psi, d_slots, off0, d_edges, eps, stats);
+            if (ss != TUSQ_OK) { cleanup(); return ss; }
+            groups.clear();
+        }
         for (const SGroup &g : groups) {
             // ---- transition to the group's core (uncompute to the divergence slot, then forward)
             const Leaf &l = core[g.l0 - lb];

@@ -677,8 +677,12 @@ __device__ __forceinline__ void issue_tile(V *smbase, uint64_t *mbar, const V *p
 __device__ __forceinline__ uint64_t dep_add(uint64_t x, uint64_t dy, uint64_t m) { return ((x | ~m) + dy) & m; }
 
 template <typename R>
-__global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename CV<R>::T *__restrict__ psi,
-                                                      const __grid_constant__ Params P, double *__restrict__ sums)
+// src: the state in the read layout; dst: where the write layout goes.  A sweep that keeps the
+// layout (every tile writes back exactly the block it read) runs in place (src == dst); one that
+// changes it is a global permutation and runs out of place into the other buffer.
+__global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const typename CV<R>::T *src,
+                                                      typename CV<R>::T *dst, const __grid_constant__ Params P,
+                                                      double *__restrict__ sums)
 {
     using V = typename CV<R>::T;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -731,7 +735,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
     for (int b = 0; b < NTB; ++b) gt |= (uint64_t)((tid >> b) & 1u) << P.pin[b];
     // the first NBUF tiles: tile j is issued by group j % NG
     for (uint64_t j = grp; j < NBUF; j += NG)
-        issue_tile(smbase, mbar, psi, j, pdep_outer(cta_tile(j), P.outer), P, gt, tid, init);
+        issue_tile(smbase, mbar, src, j, pdep_outer(cta_tile(j), P.outer), P, gt, tid, init);
     V a[NR];
     // thread parts of the phase-0 logical index (predicates, init) and of the last phase's write address
     uint64_t gthr0 = 0, gthr_st = 0;
@@ -781,7 +785,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
         }
         if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: release the buffer right away
             named_bar(bar);
-            issue_tile(smbase, mbar, psi, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
+            issue_tile(smbase, mbar, src, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
         }
 
         // ONE flat loop over records; a phase change is just a record (C_XPOSE) so that all paths
@@ -842,7 +846,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
                 }
                 if (gi == P.last_xpose) {   // the buffer is free until tile j + NBUF: hand it over
                     named_bar(bar);
-                    issue_tile(smbase, mbar, psi, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
+                    issue_tile(smbase, mbar, src, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
                 }
             }
         }
@@ -859,7 +863,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(typename C
             }
         }
         // xout has no tile bits: register offsets are additive
-        V *q0 = psi + ((bout | gthr_st) ^ P.xout);
+        V *q0 = dst + ((bout | gthr_st) ^ P.xout);
         if (P.st_pair) {
             switch (P.st_pair) {
 #define TQ_SP(v) case v: if constexpr (v < NR) store_pairs<v>(q0, a, P); break;
@@ -1948,10 +1952,21 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         fill(n_ >= 64 ? ~0ull : (1ull << n_) - 1);   // then the lowest unused qubits
         tiles[k] = t;
     }
+    // A sweep that changes the layout is a global permutation of the state: it must run out of
+    // place (alt_, the caller-provided second buffer).  Buffers alternate from ctx.psi, so the
+    // number of layout-changing sweeps must be even for the state to end in ctx.psi: with an odd
+    // number of groups, boundary 1 keeps the identity (group 0 runs in place).  Without a second
+    // buffer every layout is the identity and every sweep runs in place.
     std::vector<std::array<uint8_t, 64>> lay(NLG + 1);
+#ifdef TUSQ_DEBUG_KNOBS   // debug builds only: TUSQ_DBG_IDENTITY=1 keeps every layout the identity
+    static const bool dbg_identity = getenv("TUSQ_DBG_IDENTITY") != nullptr;
+#else
+    constexpr bool dbg_identity = false;
+#endif
+    const bool remap = alt_ != nullptr && !dbg_identity && NLG >= 2;
     for (size_t k = 0; k <= NLG; ++k) {
         auto &L = lay[k];
-        if (k == 0 || k == NLG) {
+        if (k == 0 || k == NLG || !remap) {
             for (uint32_t q = 0; q < 64; ++q) L[q] = (uint8_t)q;
             continue;
         }
@@ -1960,12 +1975,21 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         for (uint64_t part : {a & b, b & ~a, a & ~b, all & ~(a | b)})
             for (uint64_t m = part; m; m &= m - 1) L[__builtin_ctzll(m)] = pos++;
     }
+    // parity: reset remapped boundaries to the identity, first to last, until the number of
+    // layout changes is even (all-identity is even, so this terminates)
+    for (size_t k = 1; k < NLG; ++k) {
+        size_t changes = 0;
+        for (size_t j = 0; j < NLG; ++j) changes += lay[j] != lay[j + 1];
+        if (!(changes & 1)) break;
+        for (uint32_t q = 0; q < 64; ++q) lay[k][q] = (uint8_t)q;
+    }
     auto permute = [&](uint64_t x, const std::array<uint8_t, 64> &L) {
         uint64_t o = 0;
         for (; x; x &= x - 1) o |= bit(L[__builtin_ctzll(x)]);
         return o;
     };
     size_t lk = 0;   // launched-group counter
+    void *cur = ctx.psi;   // the buffer holding the state in layout lay[lk]
     for (size_t gi = 0; gi < groups.size(); ++gi) {
         const Group &G = groups[gi];
         if (G.ops.empty() && !pending_init) {   // pure relabel
@@ -1975,6 +1999,9 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         // loads go through shared memory (always coalesced): no load-layout phase needed
         build_params(G, n_, B, tiles[lk], lay[lk].data(), lay[lk + 1].data());
         Params &P = B.P;
+        void *src = cur;
+        void *dst = lay[lk] == lay[lk + 1] ? cur : (cur == ctx.psi ? alt_ : ctx.psi);
+        cur = dst;
         uint64_t m_load = (pending_init ? 0 : xmask_) ^ G.xb;
         P.xm_load = m_load;
         P.xm_store = m_load & ~B.tile;
@@ -2097,6 +2124,10 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         if (!ctx.dry) {
             int bps = blocks_per_sm(prec_);
             uint64_t grid = std::min<uint64_t>((P.ntiles + NG - 1) / NG, (uint64_t)device_sm_count() * bps);
+#ifdef TUSQ_DEBUG_KNOBS   // TUSQ_DBG_GRID=g caps the grid (several tiles per CTA at small n)
+            static const uint64_t dbg_grid = getenv("TUSQ_DBG_GRID") ? (uint64_t)atoll(getenv("TUSQ_DBG_GRID")) : 0;
+            if (dbg_grid) grid = std::min(grid, dbg_grid);
+#endif
             const size_t smem = smem_bytes(prec_);
             // incremental tile bases (deposited steps, read layout) and byte offsets for the kernel
             auto pdep = [&](uint64_t x) {
@@ -2124,9 +2155,11 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 }
             if (ctx.timer) ctx.timer->begin(ctx.st);
             if (prec_ == 128)
-                k_fused<double><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((double2 *)ctx.psi, P, d_sums);
+                k_fused<double><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((const double2 *)src, (double2 *)dst, P,
+                                                                           d_sums);
             else
-                k_fused<float><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((float2 *)ctx.psi, P, d_sums);
+                k_fused<float><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((const float2 *)src, (float2 *)dst, P,
+                                                                          d_sums);
             if (ctx.timer) ctx.timer->end(ctx.st, bytes);
         }
         count(ctx, bytes, true);
@@ -2134,6 +2167,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         xmask_ = P.xm_store ^ G.xa;
         if (want && sums_written) *sums_written = true;
     }
+    if (cur != ctx.psi) throw std::runtime_error("fused planner: layout parity left the state in the scratch buffer");
     return true;
 }
 

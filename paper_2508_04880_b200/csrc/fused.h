@@ -62,6 +62,9 @@ public:
                     bool *sums_written);
     // the logical state may be stored XOR-relabelled; materialize() clears the mask
     uint64_t xmask() const { return xmask_; }
+    // a second device buffer of the state's size: enables the layout-changing (out-of-place) sweeps
+    // whose tile reads are contiguous; NULL = every sweep in place
+    void set_alt(void *alt) { alt_ = alt; }
     void materialize(Ctx &ctx);
     void reset_mask() { xmask_ = 0; }
 
@@ -71,6 +74,7 @@ private:
     uint32_t tile_bits_;
     bool enabled_;
     uint64_t xmask_ = 0;
+    void *alt_ = nullptr;
     std::shared_ptr<PlanScratch> scratch_;
 };
 
@@ -82,6 +86,12 @@ bool comm_is_local(const tusq_comm *c);
 int comm_rank(const tusq_comm *c);
 int comm_nranks(const tusq_comm *c);
 tusq_status comm_allreduce_u64(tusq_comm *c, uint64_t *d, uint64_t n, cudaStream_t st, std::string &err);
+
+// batched sub-trees with on-chip state for small n (smallsim.cu): the leaf range [lb, le) in one
+// launch; draws go to d_slots (slot index - off0); the final state of leaf le-1 to psi
+uint32_t small_max_qubits(int prec);
+tusq_status run_tree_small(const tusq_tree *t, const tusq_exec *ex, uint64_t lb, uint64_t le, void *psi,
+                           uint64_t *d_slots, uint64_t off0, uint32_t *d_edges, double eps, tusq_run_stats &stats);
 
 // tusq_run_tree in TUSQ_MODE_SHARDED (sharded.cu)
 tusq_status run_tree_sharded(const tusq_tree *t, const tusq_exec *ex, uint64_t *out_slots, tusq_run_stats *stats);

@@ -387,3 +387,28 @@ def test_random_asymmetric_channels_slots(T, torch, oracle):
         ref, edge = ot.run()
         slots, _ = T.run_tree(t, 128)
         _check_slots(slots, ref, edge, 2048)
+
+
+def test_delta_study_matches_oracle(T, torch, oracle):
+    # the fidelity-deviation study (scripts/delta_study.py) at small sizes:
+    # the library's pruned / unpruned fidelities equal the oracle's (same slots up to edge draws)
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "delta_study", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts",
+                                    "delta_study.py"))
+    D = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(D)
+    assert abs(D.delta(0.9, 0.8) - 0.1 / 1.7) < 1e-15          # SPEC S:503's worked example
+    for family, n in (("bv", 6), ("adder", 6), ("bv", 10)):
+        row = D.run(family, n, 4096, 3, 0.01)
+        if family == "bv":
+            _, ops = W.bv(n)
+            ideal = W.bv_expected_output(n)
+        else:
+            _, ops = W.adder((n - 2) // 2)
+            ideal = W.adder_expected_output((n - 2) // 2)
+        for tag, prune in (("pruned", True), ("unpruned", False)):
+            slots, edge = oracle.Tree(n, ops, 0.01, 0.01, 0.01, 4096, 3, prune=prune).run()
+            f = float(np.mean(slots == np.uint64(ideal)))
+            assert abs(row[f"f_{tag}"] - f) <= edge.sum() / 4096 + 1e-15, (family, n, tag)
