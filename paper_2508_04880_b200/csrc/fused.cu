@@ -967,6 +967,10 @@ void GateTimer::flush()
     for (size_t i = 0; i < used_; ++i) {
         float ms = 0;
         cudaEventElapsedTime(&ms, a_[i], b_[i]);
+#ifdef TUSQ_DEBUG_KNOBS
+        static const bool dbg_trace = getenv("TUSQ_DBG_TRACE") != nullptr;
+        if (dbg_trace) fprintf(stderr, "[t] %zu %d %.4f\n", i, (int)cat_[i], ms);
+#endif
         if (cat_[i] == 0) {
             seconds += ms * 1e-3;
             bytes += by_[i];
@@ -1045,10 +1049,13 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
 {
     // strict: every qubit an op touches (controls, diagonals) must join the tile, so whole runs
     // stay in registers and fold; otherwise they join only while there is room
-    // Tile capacity.  Every group after the first reads a layout in which its own tile qubits sit
-    // at physical positions 0..11 (see FusedPlanner::execute_ex), so any 12 qubits make a
-    // contiguous tile; the first group reads the identity layout, so it keeps qubits 0,1,2
-    // (128-byte runs) and up to 9 others.
+    // Tile capacity: qubits 0,1,2 + up to 9 others.  Groups after the first read a layout in which
+    // their own tile qubits sit at physical positions 0..11 (FusedPlanner::execute_ex), so any 12
+    // qubits would make a contiguous tile -- but the sweep BEFORE such a group writes with runs of
+    // 2^m amplitudes, m = the qubits the two tiles share.  Keeping 0,1,2 in every tile keeps
+    // m >= 3 (128-byte write runs).  Measured on C4 batches (profiles/r2_k5_anatomy.json): 12 free
+    // qubits need 25 % fewer sweeps but each costs 38 % more (short write runs, more transposes);
+    // 9 + {0,1,2} with the remap is the fastest (-8 % vs the identity layout).
     uint64_t low = 7;
     int hi_cap = TB - 3;
     // tile qubits a group may claim beyond 0-2 (default all 9; fewer leave fillers 3, 4... in the
@@ -1082,7 +1089,10 @@ static std::vector<Group> make_groups(const std::vector<Op> &ops, bool strict)
             if (!drop[i]) kept.push_back(g.ops[i]);
         g.ops.swap(kept);
         if (!g.ops.empty() || g.xb || g.xa) groups.push_back(g);
-        if (!groups.empty()) { low = 0; hi_cap = TB; }
+#ifdef TUSQ_DEBUG_KNOBS   // TUSQ_DBG_CAP=12: any 12 tile qubits in the groups after the first
+        static const int dbg_cap = getenv("TUSQ_DBG_CAP") ? atoi(getenv("TUSQ_DBG_CAP")) : 0;
+        if (dbg_cap == 12 && !groups.empty()) { low = 0; hi_cap = TB; }
+#endif
         g = Group();
         touched = 0;
     };
@@ -2161,6 +2171,27 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 k_fused<float><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((const float2 *)src, (float2 *)dst, P,
                                                                           d_sums);
             if (ctx.timer) ctx.timer->end(ctx.st, bytes);
+#ifdef TUSQ_DEBUG_KNOBS   // TUSQ_DBG_TRACE=1: one line per K5 launch (group shape), for launch-time fits
+            static const bool dbg_trace = getenv("TUSQ_DBG_TRACE") != nullptr;
+            if (dbg_trace) {
+                int cnt[10] = {0};   // H, DK, CX-like, D, XPOSE, XY, T-pred, other, CU, CCX
+                for (uint32_t i = 0; i < P.ngate; ++i) {
+                    const uint16_t c = P.g[i].code;
+                    const int k = c < C_U ? 0 : (c >= C_DK && c < C_CX2) ? 1
+                                : ((c >= C_CX && c < C_CPH) || (c >= C_CX2 && c < C_CU)) ? 2
+                                : (c >= C_D1 && c < C_CX) ? 3 : c == C_XPOSE ? 4 : (c >= C_X && c < C_D1) ? 5
+                                : ((c >= C_TX && c <= C_TPH) || (c >= C_TDK && c < C_N)) ? 6
+                                : (c >= C_CU && c < C_CCX) ? 8 : (c >= C_CCX && c < C_TDK) ? 9 : 7;
+                    cnt[k]++;
+                }
+                int contig = 1;
+                for (int b = 0; b < TB; ++b) contig &= P.pin[b] == b;
+                fprintf(stderr, "[k5] idx %d ops %zu recs %u ph %u init %d contig %d oop %d gtab %d tile %#llx H %d DK %d CX %d D %d XP %d XY %d TP %d O %d CU %d CCX %d\n",
+                        ctx.timer ? (int)ctx.timer->pending() - 1 : -1, G.ops.size(), P.ngate, P.nphase, pending_init ? 1 : 0, contig, src != dst ? 1 : 0,
+                        P.gtab != 0xFFFFu, (unsigned long long)B.tile, cnt[0], cnt[1], cnt[2], cnt[3], cnt[4], cnt[5],
+                        cnt[6], cnt[7], cnt[8], cnt[9]);
+            }
+#endif
         }
         count(ctx, bytes, true);
         pending_init = false;

@@ -20,6 +20,7 @@ public:
     void begin(cudaStream_t st);
     void end(cudaStream_t st, double bytes, int cat = 0);
     void flush();                 // synchronizes the recorded events and accumulates
+    size_t pending() const { return used_; }
     uint64_t launches = 0;
     double seconds = 0.0, bytes = 0.0, sample_seconds = 0.0;
 

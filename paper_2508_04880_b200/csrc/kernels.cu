@@ -119,14 +119,23 @@ __global__ void __launch_bounds__(TPB) k_diag1_full(typename CV<R>::T *__restric
 template <typename R>
 __global__ void __launch_bounds__(TPB) k_cx(typename CV<R>::T *__restrict__ psi, uint64_t nq, uint32_t c, uint32_t t)
 {
+    // two independent quartets per thread per iteration (4 loads in flight before the stores)
     using V = typename CV<R>::T;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint32_t lo = c < t ? c : t, hi = c < t ? t : c;
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += stride) {
-        uint64_t k = insert0(insert0(j, lo), hi) | (1ull << c);
-        V a = psi[k], b = psi[k | (1ull << t)];
-        psi[k] = b;
-        psi[k | (1ull << t)] = a;
+    const uint64_t tb = 1ull << t;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += 2 * stride) {
+        const uint64_t k0 = insert0(insert0(j, lo), hi) | (1ull << c);
+        const bool two = j + stride < nq;
+        const uint64_t k1 = two ? insert0(insert0(j + stride, lo), hi) | (1ull << c) : k0;
+        const V a0 = __ldcs(psi + k0), b0 = __ldcs(psi + (k0 | tb));
+        const V a1 = __ldcs(psi + k1), b1 = __ldcs(psi + (k1 | tb));
+        __stcs(psi + k0, b0);
+        __stcs(psi + (k0 | tb), a0);
+        if (two) {
+            __stcs(psi + k1, b1);
+            __stcs(psi + (k1 | tb), a1);
+        }
     }
 }
 
@@ -148,19 +157,27 @@ template <typename R>
 __global__ void __launch_bounds__(TPB) k_pauli_x(typename CV<R>::T *__restrict__ psi, uint64_t nhalf, uint32_t lowbit,
                                                  uint64_t xm, uint64_t zm, Cx<R> gph)
 {
+    // two independent pairs per thread per iteration (4 loads in flight before the stores)
     using V = typename CV<R>::T;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nhalf; j += stride) {
-        uint64_t k0 = insert0(j, lowbit), k1 = k0 ^ xm;
-        V a = psi[k0], b = psi[k1];
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nhalf; j += 2 * stride) {
+        const bool two = j + stride < nhalf;
+        const uint64_t k0 = insert0(j, lowbit), k1 = k0 ^ xm;
+        const uint64_t m0 = two ? insert0(j + stride, lowbit) : k0, m1 = m0 ^ xm;
+        const V a = __ldcs(psi + k0), b = __ldcs(psi + k1);
+        const V c = __ldcs(psi + m0), d = __ldcs(psi + m1);
         // new[k0] = ph(k0) psi[k1], ph(k0) uses (k0 ^ xm) = k1
-        R s0 = (__popcll(k1 & zm) & 1) ? R(-1) : R(1);
-        R s1 = (__popcll(k0 & zm) & 1) ? R(-1) : R(1);
-        V na = cmul(gph, b), nb = cmul(gph, a);
-        na.x *= s0; na.y *= s0;
-        nb.x *= s1; nb.y *= s1;
-        psi[k0] = na;
-        psi[k1] = nb;
+        auto put = [&](uint64_t p0, uint64_t p1, const V &x, const V &y) {
+            const R s0 = (__popcll(p1 & zm) & 1) ? R(-1) : R(1);
+            const R s1 = (__popcll(p0 & zm) & 1) ? R(-1) : R(1);
+            V na = cmul(gph, y), nb = cmul(gph, x);
+            na.x *= s0; na.y *= s0;
+            nb.x *= s1; nb.y *= s1;
+            __stcs(psi + p0, na);
+            __stcs(psi + p1, nb);
+        };
+        put(k0, k1, a, b);
+        if (two) put(m0, m1, c, d);
     }
 }
 
@@ -266,7 +283,7 @@ static double gate_impl(void *psi_, uint32_t n, const Op &o, cudaStream_t st)
     }
     if (o.kind == CX) {
         uint64_t nq = N / 4;
-        k_cx<R><<<grid_for(nq, TPB, 1), TPB, 0, st>>>(psi, nq, o.q0, o.q1);
+        k_cx<R><<<grid_for(nq, TPB, 2), TPB, 0, st>>>(psi, nq, o.q0, o.q1);
         return 1.0 * N * s;
     }
     if (o.kind == CZ || o.kind == CP) {
@@ -297,7 +314,7 @@ static double pauli_impl(void *psi_, uint32_t n, uint64_t xm, uint64_t zm, cudaS
         static const double gr[4] = {1, 0, -1, 0}, gi[4] = {0, 1, 0, -1};
         uint32_t low = (uint32_t)__builtin_ctzll(xm);
         uint64_t nh = N / 2;
-        k_pauli_x<R><<<grid_for(nh, TPB, 1), TPB, 0, st>>>(psi, nh, low, xm, zm, cx_of<R>(gr[ny & 3], gi[ny & 3]));
+        k_pauli_x<R><<<grid_for(nh, TPB, 2), TPB, 0, st>>>(psi, nh, low, xm, zm, cx_of<R>(gr[ny & 3], gi[ny & 3]));
         return 2.0 * N * s;
     }
     uint32_t lowz = (uint32_t)__builtin_ctzll(zm);
