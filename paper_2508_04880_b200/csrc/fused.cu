@@ -476,17 +476,34 @@ __device__ __forceinline__ void gate_case(V (&a)[NR], const double *p, uint64_t 
         }
     } else if constexpr (C >= C_TDK) {
         // a run of controlled phases from outer/thread qubits onto one register bit (QFT ladders):
-        // the per-thread factor is a product of scalars, applied once
-        double fr = 1.0, fi = 0.0;
-        for (uint32_t k = 0; k < ga; ++k) {
-            const double *e = p + 3 * k;
-            if ((lbase >> (uint32_t)e[0]) & 1) {
-                const double nr = fr * e[1] - fi * e[2];
-                fi = fr * e[2] + fi * e[1];
-                fr = nr;
+        // the per-thread factor is a product of scalars, applied once.  Four independent partial
+        // products (k mod 4) cut the dependent complex-multiply chain (~30 links at 34 qubits) to
+        // a quarter; they are combined at the end.
+        double fr[4] = {1.0, 1.0, 1.0, 1.0}, fi[4] = {0.0, 0.0, 0.0, 0.0};
+        uint32_t k = 0;
+        for (; k + 4 <= ga; k += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double *e = p + 3 * (k + u);
+                if ((lbase >> (uint32_t)e[0]) & 1) {
+                    const double nr = fr[u] * e[1] - fi[u] * e[2];
+                    fi[u] = fr[u] * e[2] + fi[u] * e[1];
+                    fr[u] = nr;
+                }
             }
         }
-        if (fr != 1.0 || fi != 0.0) g_d1<C - C_TDK, V, R>(a, (R)fr, (R)fi);
+        for (; k < ga; ++k) {
+            const double *e = p + 3 * k;
+            if ((lbase >> (uint32_t)e[0]) & 1) {
+                const double nr = fr[0] * e[1] - fi[0] * e[2];
+                fi[0] = fr[0] * e[2] + fi[0] * e[1];
+                fr[0] = nr;
+            }
+        }
+        const double ar = fr[0] * fr[1] - fi[0] * fi[1], ai = fr[0] * fi[1] + fi[0] * fr[1];
+        const double br = fr[2] * fr[3] - fi[2] * fi[3], bi = fr[2] * fi[3] + fi[2] * fr[3];
+        const double tr = ar * br - ai * bi, ti = ar * bi + ai * br;
+        if (tr != 1.0 || ti != 0.0) g_d1<C - C_TDK, V, R>(a, (R)tr, (R)ti);
     } else if constexpr (C >= C_CCX) {
         constexpr int pb = (C - C_CCX) / 6;
         g_cx<(hdh_mask(pb, (C - C_CCX) % 6) & ~(1 << pb)), pb, V, true>(a);
@@ -1982,6 +1999,14 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         }
         const uint64_t a = tiles[k - 1], b = tiles[k], all = n_ >= 64 ? ~0ull : (1ull << n_) - 1;
         uint8_t pos = 0;
+#ifdef TUSQ_DEBUG_KNOBS   // TUSQ_DBG_WCONTIG=1: contiguous WRITES instead (group k-1's tile at 0..11)
+        static const bool wcontig = getenv("TUSQ_DBG_WCONTIG") != nullptr;
+        if (wcontig) {
+            for (uint64_t part : {a & b, a & ~b, b & ~a, all & ~(a | b)})
+                for (uint64_t m = part; m; m &= m - 1) L[__builtin_ctzll(m)] = pos++;
+            continue;
+        }
+#endif
         for (uint64_t part : {a & b, b & ~a, a & ~b, all & ~(a | b)})
             for (uint64_t m = part; m; m &= m - 1) L[__builtin_ctzll(m)] = pos++;
     }

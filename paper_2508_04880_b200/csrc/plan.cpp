@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <vector>
 
 #include "common.h"
 
@@ -61,47 +62,96 @@ void append_inverse(const tusq_tree &t, const Leaf &a, const Cursor &to, std::ve
     }
 }
 
-// Longest prefix of classical events (X, Y, Z, CX, diagonal gates) from |0..0>: the state
-// stays a single basis state times a phase, computed here exactly in double.
+// Longest prefix of a leaf's event stream whose result from |0..0> is a single basis state times a
+// phase, computed exactly on the host (the re-anchor target):
+//   - classical events: X, Y, Z, CX, and diagonal gates act on a basis state as a permutation and
+//     a phase;
+//   - blocks H(t) [classical events] H(t) -- e.g. the 15-gate Toffoli of a Cuccaro adder with its
+//     frozen Paulis -- are simulated on their few-entry support: when the block maps the current
+//     basis state to a single basis state (every other amplitude below 1e-13, i.e. rounding
+//     residue of an exact cancellation), the fold continues past it.  A Pauli error inside a core
+//     usually leaves it a superposition: the fold stops before that block's first H.
+// The device then starts from amp |index> at the returned cursor instead of replaying the prefix.
 Cursor fold_prefix(const tusq_tree &t, const Leaf &a, uint64_t *index, double *re, double *im)
 {
+    using C = std::complex<double>;
     const uint64_t L = t.gates.size();
-    uint64_t x = 0;
-    std::complex<double> amp(1.0, 0.0);
-    const std::complex<double> iu(0.0, 1.0);
+    const C iu(0.0, 1.0);
+    // apply one classical event (a gate or a Pauli) to a sparse state; false if not classical
+    auto classical = [&](const Op &o, std::vector<std::pair<uint64_t, C>> &v) -> bool {
+        for (auto &e : v) {
+            uint64_t &x = e.first;
+            C &amp = e.second;
+            const uint64_t b0 = (x >> o.q0) & 1, b1 = (x >> o.q1) & 1;
+            switch (o.kind) {
+            case I: break;
+            case X: x ^= 1ull << o.q0; break;
+            case Y: amp *= b0 ? -iu : iu; x ^= 1ull << o.q0; break;
+            case Z: if (b0) amp = -amp; break;
+            case S: if (b0) amp *= iu; break;
+            case SDG: if (b0) amp *= -iu; break;
+            case T: if (b0) amp *= C(M_SQRT1_2, M_SQRT1_2); break;
+            case TDG: if (b0) amp *= C(M_SQRT1_2, -M_SQRT1_2); break;
+            case RZ: amp *= std::exp(iu * (b0 ? 0.5 : -0.5) * o.theta); break;
+            case P: if (b0) amp *= std::exp(iu * o.theta); break;
+            case CX: if (b0) x ^= 1ull << o.q1; break;
+            case CZ: if (b0 && b1) amp = -amp; break;
+            case CP: if (b0 && b1) amp *= std::exp(iu * o.theta); break;
+            default: return false;
+            }
+        }
+        return true;
+    };
+    auto hadamard = [&](uint32_t q, std::vector<std::pair<uint64_t, C>> &v) {
+        std::vector<std::pair<uint64_t, C>> out;
+        for (auto &e : v) {
+            const uint64_t x0 = e.first & ~(1ull << q), x1 = x0 | (1ull << q);
+            const double sgn = ((e.first >> q) & 1) ? -1.0 : 1.0;
+            out.push_back({x0, e.second * M_SQRT1_2});
+            out.push_back({x1, e.second * (sgn * M_SQRT1_2)});
+        }
+        std::sort(out.begin(), out.end(), [](const auto &p, const auto &q2) { return p.first < q2.first; });
+        v.clear();
+        for (auto &e : out) {
+            if (!v.empty() && v.back().first == e.first) v.back().second += e.second;
+            else v.push_back(e);
+        }
+    };
+    std::vector<std::pair<uint64_t, C>> st{{0, C(1.0, 0.0)}};
     size_t k = 0;
     uint64_t pos = 0;
-    auto pauli = [&](uint32_t p, uint32_t q) {
-        uint64_t b = (x >> q) & 1;
-        if (p == X) x ^= 1ull << q;
-        else if (p == Y) { amp *= b ? -iu : iu; x ^= 1ull << q; }
-        else if (p == Z) { if (b) amp = -amp; }
-    };
+    auto pauli = [&](const Triple &tr) { return Op{tr.p, tr.q, 0u, 0.0}; };
     for (; pos <= L; ++pos) {
-        while (k < a.tr.size() && a.tr[k].pos == pos) { pauli(a.tr[k].p, a.tr[k].q); ++k; }
+        while (k < a.tr.size() && a.tr[k].pos == pos) { classical(pauli(a.tr[k]), st); ++k; }
         if (pos == L) break;
         const Op &o = t.gates[pos];
-        uint64_t b0 = (x >> o.q0) & 1, b1 = (x >> o.q1) & 1;
-        bool ok = true;
-        switch (o.kind) {
-        case I: break;
-        case X: case Y: case Z: pauli(o.kind, o.q0); break;
-        case S: if (b0) amp *= iu; break;
-        case SDG: if (b0) amp *= -iu; break;
-        case T: if (b0) amp *= std::complex<double>(M_SQRT1_2, M_SQRT1_2); break;
-        case TDG: if (b0) amp *= std::complex<double>(M_SQRT1_2, -M_SQRT1_2); break;
-        case RZ: amp *= std::exp(iu * (b0 ? 0.5 : -0.5) * o.theta); break;
-        case P: if (b0) amp *= std::exp(iu * o.theta); break;
-        case CX: if (b0) x ^= 1ull << o.q1; break;
-        case CZ: if (b0 && b1) amp = -amp; break;
-        case CP: if (b0 && b1) amp *= std::exp(iu * o.theta); break;
-        default: ok = false; break;
+        if (classical(o, st)) continue;
+        if (o.kind != H) break;
+        // a block H(q) ... H(q): classical events in between, on a copy of the state
+        const uint32_t q = o.q0;
+        uint64_t e = pos + 1;
+        size_t ke = k;
+        std::vector<std::pair<uint64_t, C>> w = st;
+        hadamard(q, w);
+        bool ok = false;
+        for (; e < L; ++e) {
+            while (ke < a.tr.size() && a.tr[ke].pos == e) { classical(pauli(a.tr[ke]), w); ++ke; }
+            const Op &g = t.gates[e];
+            if (g.kind == H && g.q0 == q) { hadamard(q, w); ok = true; break; }
+            if (!classical(g, w)) break;
         }
         if (!ok) break;
+        std::vector<std::pair<uint64_t, C>> keep;
+        for (auto &x : w)
+            if (std::abs(x.second) > 1e-13) keep.push_back(x);
+        if (keep.size() != 1) break;   // the block leaves a superposition: stop before its first H
+        st = keep;
+        pos = e;                        // gate e (the closing H) is done; triples at e applied
+        k = ke;
     }
-    *index = x;
-    *re = amp.real();
-    *im = amp.imag();
+    *index = st[0].first;
+    *re = st[0].second.real();
+    *im = st[0].second.imag();
     return Cursor{pos, (uint32_t)k};
 }
 

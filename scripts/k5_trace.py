@@ -58,7 +58,8 @@ def fit(rows):
 if __name__ == "__main__":
     out = {}
     variants = [("remap_cap9 (default)", {}), ("remap12", {"TUSQ_DBG_CAP": "12"}),
-                ("identity_cap9 (round 1)", {"TUSQ_DBG_IDENTITY": "1"})]
+                ("identity_cap9 (round 1)", {"TUSQ_DBG_IDENTITY": "1"}),
+                ("remap_wcontig", {"TUSQ_DBG_WCONTIG": "1"})]
     if os.environ.get("K5T_ONLY_DEFAULT"):
         variants = variants[:1]
     for name, env in variants:

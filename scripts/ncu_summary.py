@@ -23,6 +23,7 @@ KEYS = {
     "launch__grid_size": "grid_size",
     "launch__block_size": "block_size",
     "launch__shared_mem_per_block_dynamic": "dyn_smem_bytes",
+    "dram__bytes_read.sum.per_second": "dram_read_bytes_per_s",
     "smsp__average_warp_latency_issue_stalled_barrier": "stall_barrier",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "smem_wavefronts",
@@ -33,8 +34,11 @@ def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], dict(zip(rows[0], rows[1]))
+    # ncu prints memory sizes in decimal (Kbyte = 1e3 B) and shared-memory sizes in binary units
+    # (KiB, "Kibyte"): both are scaled to plain bytes here
     scale = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6,
-             "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+             "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+             "Kibyte": 1024, "Mibyte": 1 << 20, "Gibyte": 1 << 30, "KB": 1e3, "KiB": 1024, "MiB": 1 << 20}
     res = []
     for r in rows[2:]:
         d = dict(zip(hdr, r))
@@ -42,7 +46,10 @@ def raw(rep):
         for k, name in KEYS.items():
             if k in d and d[k] not in ("", "n/a"):
                 try:
-                    e[name] = float(d[k].replace(",", "")) * scale.get(units.get(k, ""), 1)
+                    unit = units.get(k, "")
+                    if unit.endswith("/block"):   # e.g. dynamic shared memory in "Kbyte/block"
+                        unit = unit[:-len("/block")]
+                    e[name] = float(d[k].replace(",", "")) * scale.get(unit, 1)
                 except ValueError:
                     e[name] = d[k]
         res.append(e)
