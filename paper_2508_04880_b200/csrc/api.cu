@@ -247,15 +247,9 @@ tusq_status tusq_apply_ops(void *d_state, uint32_t n, uint32_t precision, const 
     ctx.psi = d_state; ctx.n = n; ctx.prec = (int)precision; ctx.st = (cudaStream_t)stream; ctx.stats = &stats;
     ctx.dry = (flags & TUSQ_APPLY_PLAN_ONLY) != 0;
     FusedPlanner planner(n, (int)precision);
-    void *alt = nullptr;
     const bool fused = !(flags & TUSQ_APPLY_UNFUSED) && planner.enabled();
-    if (fused && !ctx.dry && L > 0) {   // second buffer for the layout-changing sweeps (optional)
-        if (cudaMallocAsync(&alt, (precision == 128 ? 16ull : 8ull) << n, ctx.st) != cudaSuccess) {
-            cudaGetLastError();
-            alt = nullptr;
-        }
-        planner.set_alt(alt);
-    }
+    // second buffer for the layout-changing sweeps: allocated only if the ops form >= 2 groups
+    if (fused) planner.set_alt_lazy((precision == 128 ? 16ull : 8ull) << n);
     try {
         if (fused) {
             planner.execute(v, ctx);
@@ -264,10 +258,10 @@ tusq_status tusq_apply_ops(void *d_state, uint32_t n, uint32_t precision, const 
             execute_unfused(v, ctx);
         }
     } catch (const std::exception &e) {
-        if (alt) cudaFreeAsync(alt, ctx.st);
+        planner.release(ctx.st);
         return fail(TUSQ_ERR_INTERNAL, e.what());
     }
-    if (alt) cudaFreeAsync(alt, ctx.st);
+    planner.release(ctx.st);
     if (!ctx.dry) TQ_CUDA(cudaGetLastError());
     return TUSQ_OK;
 }
@@ -443,6 +437,9 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     ops.reserve(4 * t->gates.size() + 64);
     uint64_t since_anchor = 0;
     bool phys_sums_valid = false;
+    bool virt = false;                 // the device state is the basis state vstate, not yet written
+    InitState vstate{0, 1.0, 0.0};
+    std::vector<uint64_t> fills;       // (slot - off0, count, value) of the virtual leaves' draws
     try {
         if (small) {
             tusq_status ss = run_tree_small(t, ex, lb, le, psi, d_slots, off0, d_edges, eps, stats);
@@ -475,6 +472,29 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
                 since_anchor = ops.size();
             }
             stats.gate_apps += ops.size();
+            // A leaf whose whole executed stream folds (reset with nothing left to apply) is the basis
+            // state amp|x>: it stays VIRTUAL -- no device pass -- and its draws are x ^ readout mask
+            // (a single-outcome CDF: every draw picks x exactly).  A later uncompute from it starts
+            // by resetting to that basis state, fused into its first sweep.
+            if (reset && ops.empty()) {
+                virt = true;
+                vstate = init;
+                phys_sums_valid = false;
+                if (sample)
+                    for (uint64_t li = g.l0; li < g.l1; ++li)
+                        if (t->leaves[li].count) {
+                            fills.push_back(t->leaves[li].offset - off0);
+                            fills.push_back(t->leaves[li].count);
+                            fills.push_back(init.index ^ tmask[li - lb]);
+                            stats.draws += t->leaves[li].count;
+                        }
+                stats.leaves += g.l1 - g.l0;
+                stats.sampled_vectors++;
+                continue;
+            }
+            const bool from_virtual = virt && !reset;   // uncompute from a basis state never written
+            if (from_virtual) { reset = true; init = vstate; }
+            virt = false;
             const uint64_t sweeps_before = stats.sweeps;
             uint64_t draws = 0;
             for (uint64_t li = g.l0; li < g.l1; ++li) draws += t->leaves[li].count;
@@ -532,7 +552,22 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
                 }
             }
         }
+        if (virt) {   // the call ends on a virtual leaf: write its basis state (K7)
+            if (!dry) launch_init_basis(psi, n, prec, vstate.index, vstate.re, vstate.im, st);
+            stats.launches++;
+            stats.hbm_bytes += (double)need;
+            if (fuse) planner.reset_mask();
+        }
         if (fuse) planner.materialize(ctx);   // leave the caller's buffer in logical order
+        if (!dry && !fills.empty()) {   // the virtual leaves' draws, one launch
+            void *fb = nullptr;
+            TQ_RUN_CUDA(scratch_alloc(&fb, fills.size() * 8, st));
+            TQ_RUN_CUDA(cudaMemcpyAsync(fb, fills.data(), fills.size() * 8, cudaMemcpyHostToDevice, st));
+            launch_fill_slots((const uint64_t *)fb, fills.size() / 3, d_slots, st);
+            TQ_RUN_CUDA(cudaFreeAsync(fb, st));
+            stats.launches++;
+            stats.h2d_bytes += (double)fills.size() * 8;
+        }
         if (!dry) {
             TQ_RUN_CUDA(cudaEventRecord(ev[1], st));
             if (comm && sample) {   // the disjoint slot arrays of all ranks, summed on the device

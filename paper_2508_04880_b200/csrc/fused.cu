@@ -1990,6 +1990,10 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
 #else
     constexpr bool dbg_identity = false;
 #endif
+    if (!alt_ && alt_lazy_ && NLG >= 2 && !ctx.dry && !dbg_identity) {
+        if (cudaMallocAsync(&alt_, alt_lazy_, ctx.st) == cudaSuccess) alt_owned_ = true;
+        else { cudaGetLastError(); alt_ = nullptr; alt_lazy_ = 0; }   // no memory: stay in place
+    }
     const bool remap = alt_ != nullptr && !dbg_identity && NLG >= 2;
     for (size_t k = 0; k <= NLG; ++k) {
         auto &L = lay[k];

@@ -66,6 +66,14 @@ public:
     // a second device buffer of the state's size: enables the layout-changing (out-of-place) sweeps
     // whose tile reads are contiguous; NULL = every sweep in place
     void set_alt(void *alt) { alt_ = alt; }
+    // or: allocate it (stream-ordered, `bytes`) only when a call has >= 2 groups; release() frees it
+    void set_alt_lazy(uint64_t bytes) { alt_lazy_ = bytes; }
+    void release(cudaStream_t st)
+    {
+        if (alt_owned_ && alt_) cudaFreeAsync(alt_, st);
+        if (alt_owned_) alt_ = nullptr;
+        alt_owned_ = false;
+    }
     void materialize(Ctx &ctx);
     void reset_mask() { xmask_ = 0; }
 
@@ -76,6 +84,8 @@ private:
     bool enabled_;
     uint64_t xmask_ = 0;
     void *alt_ = nullptr;
+    uint64_t alt_lazy_ = 0;
+    bool alt_owned_ = false;
     std::shared_ptr<PlanScratch> scratch_;
 };
 

@@ -638,4 +638,21 @@ double launch_draws_window(const void *psi, uint32_t n, int prec, uint32_t block
     return (double)n_draws * (double)(1ull << block_bits) * (prec == 64 ? 8.0 : 16.0);
 }
 
+// draws of leaves whose state is a known basis state (every draw = that index ^ readout mask):
+// trip = ntrip (slot offset, count, value) triples, one warp per triple
+__global__ void __launch_bounds__(TPB) k_fill_slots(const uint64_t *__restrict__ trip, uint64_t ntrip,
+                                                    uint64_t *__restrict__ slots)
+{
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= ntrip) return;
+    const uint64_t off = trip[3 * w], cnt = trip[3 * w + 1], val = trip[3 * w + 2];
+    for (uint64_t j = threadIdx.x & 31; j < cnt; j += 32) slots[off + j] = val;
+}
+
+void launch_fill_slots(const uint64_t *d_trip, uint64_t ntrip, uint64_t *d_slots, cudaStream_t st)
+{
+    if (!ntrip) return;
+    k_fill_slots<<<(unsigned)((ntrip * 32 + TPB - 1) / TPB), TPB, 0, st>>>(d_trip, ntrip, d_slots);
+}
+
 }  // namespace tq

@@ -35,6 +35,9 @@ double launch_draws_window(const void *psi, uint32_t n, int prec, uint32_t block
                            double edge_eps, uint64_t *d_out, uint32_t *d_edges, double t_total, double t_lo,
                            double t_hi, uint64_t ohi, cudaStream_t st);
 
+// slots of leaves whose state is a basis state: ntrip (slot offset, count, value) triples (device)
+void launch_fill_slots(const uint64_t *d_trip, uint64_t ntrip, uint64_t *d_slots, cudaStream_t st);
+
 int device_sm_count();
 
 }  // namespace tq
