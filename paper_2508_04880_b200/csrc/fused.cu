@@ -126,7 +126,8 @@ constexpr int NCH = 4;             // 8-bit chunks of the tile index (n <= TB + 
 struct Params {
     uint64_t xm_load, xm_store;   // logical X-relabel mask at load / at store (outer bits only)
     uint64_t xin, xout;           // xm_store in the read / write layout
-    uint64_t init_index;          // F_INIT: virtual memory holds init amp at physical init_index
+    uint64_t init_tile;           // F_INIT: the state is init_re + i init_im at ONE element: register
+    uint32_t init_t, init_r;      //   init_r of thread init_t of tile init_tile (phase-0 layout), 0 elsewhere
     double init_re, init_im;
     double scale_re, scale_im;
     uint64_t ntiles;
@@ -720,7 +721,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
     // tile index -> write-layout / logical base: one table per 8-bit chunk of the tile index
     uint64_t(*tabo)[256] = reinterpret_cast<uint64_t(*)[256]>(gsm + NR * NT);
     uint64_t(*tabl)[256] = tabo + NCH;
-    const bool need_l = P.flags & (F_LBASE | F_INIT);
+    const bool need_l = P.flags & F_LBASE;
     for (uint32_t i = threadIdx.x; i < NCH * 256; i += NT * NG) {
         const uint32_t c = i >> 8, v = i & 255u;
         uint64_t o = 0, l = 0;
@@ -774,17 +775,16 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         char *smb = reinterpret_cast<char *>(sm);
         const uint64_t bout = lookup(tabo, T);
         const uint64_t blog = need_l ? lookup(tabl, T) : 0;
-        const uint64_t gthr = gthr0;
         mbar_wait(&mbar[j % NBUF], (uint32_t)((j / NBUF) & 1));
         if (init) {
-            // the same addressing as a load, from a virtual memory holding init at init_index
-            // (a reset group reads the identity layout: logical = physical positions)
-            const uint64_t lt = ((blog | gthr) ^ P.xm_load) & ~P.regm_load;
+            // a reset: every amplitude is 0 but one, whose place in the phase-0 layout (after any
+            // leading transposes, folded away on the host) the planner computed
 #pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                const bool hit = (lt + P.gl[r]) == P.init_index;
-                a[r].x = hit ? (R)P.init_re : R(0);
-                a[r].y = hit ? (R)P.init_im : R(0);
+            for (int r = 0; r < NR; ++r) { a[r].x = R(0); a[r].y = R(0); }
+            if (T == P.init_tile && tid == P.init_t) {
+#pragma unroll
+                for (int r = 0; r < NR; ++r)
+                    if ((uint32_t)r == P.init_r) { a[r].x = (R)P.init_re; a[r].y = (R)P.init_im; }
             }
         } else {
             // the tile has landed in shared memory in logical order: read it in the phase-0 layout
@@ -2097,7 +2097,50 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             P.gtab = 0xFFFFu;
             uint32_t kstar = 0;
             while (kstar < P.ngate && P.g[kstar].code == C_XPOSE) ++kstar;
-            if (!pending_init && kstar > 0 && B.prm_used + NR * NT / 4 <= (size_t)MAXP) {
+            // A reset group holds ONE nonzero element: its leading transposes fold away entirely
+            // -- the host follows that element through them (the same slot simulation as the
+            // gather) and the kernel puts it straight into its final register.
+            if (pending_init) {
+                auto &V = scratch_->V;
+                auto &M = scratch_->M;
+                auto tt = [&](const Phase &ph, uint32_t t) {
+                    uint32_t x = 0;
+                    for (int j = 0; j < NTB; ++j) x |= ((t >> j) & 1u) << ph.tl[j];
+                    return swz(x);
+                };
+                for (uint32_t t = 0; t < (uint32_t)NT; ++t)
+                    for (int r = 0; r < NR; ++r) V[t][r] = (uint16_t)(tt(P.ph[0], t) ^ P.ph[0].so[r]);
+                uint32_t cur = 0;
+                for (uint32_t k = 0; k < kstar; ++k) {
+                    const Phase &a = P.ph[cur], &b = P.ph[P.g[k].a];
+                    for (uint32_t t = 0; t < (uint32_t)NT; ++t)
+                        for (int r = 0; r < NR; ++r) M[tt(a, t) ^ a.so_out[r]] = V[t][r];
+                    for (uint32_t t = 0; t < (uint32_t)NT; ++t)
+                        for (int r = 0; r < NR; ++r) V[t][r] = M[tt(b, t) ^ b.so[r]];
+                    cur = P.g[k].a;
+                }
+                // the nonzero logical element l* (the reset target seen through the load mask), its
+                // tile and its tile-local index; find the register that holds it
+                const uint64_t lstar = init->index ^ m_load;
+                uint32_t estar = 0;
+                for (int b = 0; b < TB; ++b) estar |= (uint32_t)((lstar >> P.qs[b]) & 1u) << b;
+                P.init_tile = 0;
+                for (uint32_t k = 0; k < P.nout; ++k) P.init_tile |= ((lstar >> P.ol[k]) & 1ull) << k;
+                const uint16_t want = (uint16_t)swz(estar);
+                bool found = false;
+                for (uint32_t t = 0; t < (uint32_t)NT && !found; ++t)
+                    for (int r = 0; r < NR && !found; ++r)
+                        if (V[t][r] == want) { P.init_t = t; P.init_r = (uint32_t)r; found = true; }
+                if (!found) throw std::runtime_error("fused planner: reset element not found");
+                for (uint32_t k = cur; k < P.nphase; ++k) P.ph[k - cur] = P.ph[k];
+                P.nphase -= cur;
+                for (uint32_t i = kstar; i < P.ngate; ++i) {
+                    P.g[i - kstar] = P.g[i];
+                    if (P.g[i - kstar].code == C_XPOSE) P.g[i - kstar].a = (uint8_t)(P.g[i - kstar].a - cur);
+                }
+                P.ngate -= kstar;
+                if (P.ngate < (uint32_t)MAXG) P.g[P.ngate] = GRec{};
+            } else if (kstar > 0 && B.prm_used + NR * NT / 4 <= (size_t)MAXP) {
                 auto &V = scratch_->V;
                 auto &M = scratch_->M;
                 auto tt = [&](const Phase &ph, uint32_t t) {
@@ -2143,7 +2186,6 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         }
         if (pending_init) {
             P.flags |= F_INIT;
-            P.init_index = init->index;
             P.init_re = init->re;
             P.init_im = init->im;
         }
