@@ -114,7 +114,7 @@ struct GRec {
     uint16_t _pad;
 };
 
-enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8 };
+enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8, F_BULK = 16 };
 constexpr int NCH = 4;             // 8-bit chunks of the tile index (n <= TB + 8 * NCH = 44 fused)
 
 // Qubit layout: the state may be stored with its qubits permuted (logical qubit q at physical bit
@@ -151,6 +151,7 @@ struct Params {
     // the host plans): the kernel adds them to byte pointers with no index scaling
     uint64_t gj[NR];              // global offset of tile-local index (j << NTB) (copy slots)
     uint16_t sj[NR];              // swz(j << NTB): swizzled shared-memory part of copy slot j
+    uint16_t so0[NR];             // F_BULK: phase-0 read offsets (bytes) into the LINEAR tile buffer
     uint64_t gl[NR];              // phase 0: global element offset of register r (additive)
     uint64_t gs[NR];              // last phase: global offset of register r (additive)
     Phase ph[MAXPH];
@@ -684,11 +685,27 @@ __device__ __forceinline__ void issue_tile(V *smbase, uint64_t *mbar, const V *p
     const int b = (int)(j % NBUF);
     if (init) {
         mbar_arrive(&mbar[b]);
+    } else if (P.flags & F_BULK) {
+        // the tile is one contiguous 64 KiB (c128) block: ONE bulk copy (TMA engine, UBLKCP)
+        // issued by one thread, completion as transaction bytes on the buffer's mbarrier
+        if (tid == 0) {
+            constexpr uint32_t bytes = (1u << TB) * (uint32_t)sizeof(V);
+            const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar[b]);
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(smbase + (size_t)b * (1u << TB));
+            const V *src = psi + (tbase ^ P.xin);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(dst), "l"(src), "r"(bytes), "r"(mb)
+                         : "memory");
+        }
     } else {
         prefetch_tile(smbase + (size_t)b * (1u << TB), psi, tbase, P, gt, tid);
         mbar_arrive_cp_async(&mbar[b]);
     }
 }
+
+// before a buffer written through the generic proxy (transposes) is refilled by the async proxy
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // tile bases step in the deposited (outer-bit) domain: filling the holes with ones lets the
 // carries of an ordinary add run through them (pdep(x + y) = ((pdep x | ~m) + pdep y) & m)
@@ -737,7 +754,10 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         tabl[c][v] = l;
     }
     if (threadIdx.x == 0) {
-        for (int b = 0; b < NBUF; ++b) mbar_init(&mbar[b], NT);
+        // arrivals per phase: one expect_tx arrival per bulk copy, or every thread's cp.async
+        // arrival / reset arrival
+        const uint32_t cnt = (P.flags & F_BULK) ? 1u : (uint32_t)NT;
+        for (int b = 0; b < NBUF; ++b) mbar_init(&mbar[b], cnt);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -791,6 +811,13 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
             if (P.gtab != 0xFFFFu) {
 #pragma unroll
                 for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + gsm[r * NT + tid]);
+            } else if (P.flags & F_BULK) {   // linear buffer: logical element e at slot e ^ mloc
+                uint32_t t0 = 0;
+#pragma unroll
+                for (int q = 0; q < NTB; ++q) t0 |= ((tid >> q) & 1u) << P.ph[0].tl[q];
+                t0 *= (uint32_t)sizeof(V);
+#pragma unroll
+                for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + (t0 ^ P.so0[r]));
             } else {
                 uint32_t t0 = 0;
 #pragma unroll
@@ -801,6 +828,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
             }
         }
         if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: release the buffer right away
+            if (P.flags & F_BULK) fence_proxy_async();
             named_bar(bar);
             issue_tile(smbase, mbar, src, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
         }
@@ -862,6 +890,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                     for (int q = 0; q < NTB; ++q) lbase |= (uint64_t)((tid >> q) & 1u) << P.qs[cur.tl[q]];
                 }
                 if (gi == P.last_xpose) {   // the buffer is free until tile j + NBUF: hand it over
+                    if (P.flags & F_BULK) fence_proxy_async();
                     named_bar(bar);
                     issue_tile(smbase, mbar, src, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
                 }
@@ -2047,6 +2076,10 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         P.xin = permute(P.xm_store, lay[lk]);
         P.xout = permute(P.xm_store, lay[lk + 1]);
         ++lk;
+        // a contiguous tile (its 12 qubits at read positions 0..11) loads with one bulk copy into a
+        // LINEAR buffer; otherwise per-thread cp.async into the swizzled layout
+        bool bulk = !pending_init;
+        for (int b = 0; b < TB && bulk; ++b) bulk = P.pin[b] == b;
         {
             const Phase &f = P.ph[0], &l = P.ph[P.nphase - 1];
             P.regm_load = 0;
@@ -2148,8 +2181,13 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                     for (int j = 0; j < NTB; ++j) x |= ((t >> j) & 1u) << ph.tl[j];
                     return swz(x);
                 };
+                // initial slot of the element (t, r) reads in phase 0: swizzled (cp.async copy) or
+                // linear with the tile part of the load mask (bulk copy; swz is an involution)
                 for (uint32_t t = 0; t < (uint32_t)NT; ++t)
-                    for (int r = 0; r < NR; ++r) V[t][r] = (uint16_t)(tt(P.ph[0], t) ^ P.ph[0].so[r]);
+                    for (int r = 0; r < NR; ++r) {
+                        const uint16_t sw = (uint16_t)(tt(P.ph[0], t) ^ P.ph[0].so[r]);
+                        V[t][r] = bulk ? (uint16_t)(swz(sw) ^ P.mloc) : sw;
+                    }
                 uint32_t cur = 0;
                 for (uint32_t k = 0; k < kstar; ++k) {
                     const Phase &a = P.ph[cur], &b = P.ph[P.g[k].a];
@@ -2177,6 +2215,8 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             P.last_xpose = 0xFFFFu;
             for (uint32_t i = 0; i < P.ngate; ++i)
                 if (P.g[i].code == C_XPOSE) P.last_xpose = (uint16_t)i;
+            // linear phase-0 read offsets of the bulk path (element units; bytes below)
+            for (int r = 0; r < NR; ++r) P.so0[r] = (uint16_t)(swz(P.ph[0].so[r]) ^ P.mloc);
         }
         P.ntiles = 1ull << (n_ - TB);
         P.flags = 0;
@@ -2184,6 +2224,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             const uint16_t c = P.g[i].code;
             if ((c >= C_TX && c <= C_TPH) || (c >= C_TDK && c < C_N)) P.flags |= F_LBASE;
         }
+        if (bulk) P.flags |= F_BULK;
         if (pending_init) {
             P.flags |= F_INIT;
             P.init_re = init->re;
@@ -2228,6 +2269,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 P.gs[r] *= esz;
                 P.gj[r] *= esz;
                 P.sj[r] = (uint16_t)(P.sj[r] * esz);
+                P.so0[r] = (uint16_t)(P.so0[r] * esz);
             }
             for (uint32_t k = 0; k < P.nphase; ++k)
                 for (int r = 0; r < NR; ++r) {
