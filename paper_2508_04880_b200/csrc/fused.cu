@@ -52,6 +52,12 @@ constexpr int MAXPH = 24;
 #endif
 constexpr int NG = TQ_NG;      // tile groups (of NT threads) per CTA
 constexpr int NBUF = TQ_NBUF;  // tile buffers per CTA (shared memory)
+// One mbarrier per (buffer, group) pair, i.e. per tile index mod NBUF * NG: the tiles of a buffer
+// alternate between the groups, and with one barrier per buffer a group could wait on the phase
+// two ahead of the one in flight and see its parity as already complete (phase aliasing; it let a
+// group read a tile still landing and over-arrive on the barrier -- a launch failure at 24q).
+// Per pair, every barrier has ONE consumer that waits its phases in order.
+constexpr int NMB = NBUF * NG;
 constexpr int MAXG = 400;
 constexpr int MAXP = 1600;
 
@@ -684,15 +690,23 @@ __device__ __forceinline__ void issue_tile(V *smbase, uint64_t *mbar, const V *p
     if (cta_tile(j) >= P.ntiles) return;
     const int b = (int)(j % NBUF);
     if (init) {
-        mbar_arrive(&mbar[b]);
+        mbar_arrive(&mbar[j % NMB]);
     } else if (P.flags & F_BULK) {
         // the tile is one contiguous 64 KiB (c128) block: ONE bulk copy (TMA engine, UBLKCP)
         // issued by one thread, completion as transaction bytes on the buffer's mbarrier
         if (tid == 0) {
             constexpr uint32_t bytes = (1u << TB) * (uint32_t)sizeof(V);
-            const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar[b]);
+            const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar[j % NMB]);
             const unsigned dst = (unsigned)__cvta_generic_to_shared(smbase + (size_t)b * (1u << TB));
             const V *src = psi + (tbase ^ P.xin);
+#ifdef TUSQ_DEBUG_CHECKS
+            if (((tbase ^ P.xin) & ((1u << TB) - 1)) || (tbase ^ P.xin) >= (P.ntiles << TB)) {
+                printf("k_fused bulk: bad tile base %llx (xin %llx, ntiles %llu) block %d j %llu\n",
+                       (unsigned long long)tbase, (unsigned long long)P.xin, (unsigned long long)P.ntiles,
+                       (int)blockIdx.x, (unsigned long long)j);
+                __trap();
+            }
+#endif
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                          ::"r"(dst), "l"(src), "r"(bytes), "r"(mb)
@@ -700,7 +714,7 @@ __device__ __forceinline__ void issue_tile(V *smbase, uint64_t *mbar, const V *p
         }
     } else {
         prefetch_tile(smbase + (size_t)b * (1u << TB), psi, tbase, P, gt, tid);
-        mbar_arrive_cp_async(&mbar[b]);
+        mbar_arrive_cp_async(&mbar[j % NMB]);
     }
 }
 
@@ -722,7 +736,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
     using V = typename CV<R>::T;
     extern __shared__ __align__(16) unsigned char smraw[];
     V *smbase = reinterpret_cast<V *>(smraw);
-    __shared__ uint64_t mbar[NBUF];
+    __shared__ uint64_t mbar[NMB];
     __shared__ double red[NG][NT / 32];
     const uint32_t grp = threadIdx.x / NT;
     const uint32_t tid = threadIdx.x % NT;
@@ -757,7 +771,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         // arrivals per phase: one expect_tx arrival per bulk copy, or every thread's cp.async
         // arrival / reset arrival
         const uint32_t cnt = (P.flags & F_BULK) ? 1u : (uint32_t)NT;
-        for (int b = 0; b < NBUF; ++b) mbar_init(&mbar[b], cnt);
+        for (int b = 0; b < NMB; ++b) mbar_init(&mbar[b], cnt);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -795,13 +809,17 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         char *smb = reinterpret_cast<char *>(sm);
         const uint64_t bout = lookup(tabo, T);
         const uint64_t blog = need_l ? lookup(tabl, T) : 0;
-        mbar_wait(&mbar[j % NBUF], (uint32_t)((j / NBUF) & 1));
+        mbar_wait(&mbar[j % NMB], (uint32_t)((j / NMB) & 1));
+        // A reset sweep holds ONE nonzero element, in tile init_tile; the group's gates act inside
+        // tiles (outer qubits only as predicates), so every other tile is zero before and after
+        // them: those tiles skip the records and just store their zeros.
+        const bool zero_tile = init && T != P.init_tile;
         if (init) {
             // a reset: every amplitude is 0 but one, whose place in the phase-0 layout (after any
             // leading transposes, folded away on the host) the planner computed
 #pragma unroll
             for (int r = 0; r < NR; ++r) { a[r].x = R(0); a[r].y = R(0); }
-            if (T == P.init_tile && tid == P.init_t) {
+            if (!zero_tile && tid == P.init_t) {
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
                     if ((uint32_t)r == P.init_r) { a[r].x = (R)P.init_re; a[r].y = (R)P.init_im; }
@@ -827,7 +845,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                 for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + (t0 ^ P.ph[0].so[r]));
             }
         }
-        if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: release the buffer right away
+        if (P.last_xpose == 0xFFFFu || zero_tile) {   // no transpose in this group: release the buffer right away
             if (P.flags & F_BULK) fence_proxy_async();
             named_bar(bar);
             issue_tile(smbase, mbar, src, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
@@ -842,8 +860,9 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         // -> branch chain was the top stall in ncu's source view; a shared-memory copy fetched by
         // a volatile load at the top of the iteration measured ~6 % slower)
         const uint64_t *recw = reinterpret_cast<const uint64_t *>(P.g);
-        uint64_t wnext = P.ngate ? recw[0] : 0;
-        for (uint32_t gi = 0; gi < P.ngate; ++gi) {
+        const uint32_t ngate = zero_tile ? 0u : P.ngate;
+        uint64_t wnext = ngate ? recw[0] : 0;
+        for (uint32_t gi = 0; gi < ngate; ++gi) {
             const uint64_t w = wnext;
             wnext = recw[gi + 1 < P.ngate ? gi + 1 : gi];
             GRec g;
@@ -910,6 +929,13 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         }
         // xout has no tile bits: register offsets are additive
         V *q0 = dst + ((bout | gthr_st) ^ P.xout);
+#ifdef TUSQ_DEBUG_CHECKS
+        for (int r = 0; r < NR; ++r)
+            if (((bout | gthr_st) ^ P.xout) + P.gs[r] / sizeof(V) >= (P.ntiles << TB)) {
+                printf("k_fused store: out of range (tile %llu, reg %d)\n", (unsigned long long)T, r);
+                __trap();
+            }
+#endif
         if (P.st_pair) {
             switch (P.st_pair) {
 #define TQ_SP(v) case v: if constexpr (v < NR) store_pairs<v>(q0, a, P); break;
