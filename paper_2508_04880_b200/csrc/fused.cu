@@ -120,7 +120,7 @@ struct GRec {
     uint16_t _pad;
 };
 
-enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8, F_BULK = 16 };
+enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8, F_BULK = 16, F_ONE = 32 };
 constexpr int NCH = 4;             // 8-bit chunks of the tile index (n <= TB + 8 * NCH = 44 fused)
 
 // Qubit layout: the state may be stored with its qubits permuted (logical qubit q at physical bit
@@ -675,10 +675,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t parity)
                  : "memory");
 }
 
-// tile index of this CTA's j-th tile
-__device__ __forceinline__ uint64_t cta_tile(uint64_t j)
+// tile index of this CTA's j-th tile, or ~0 past the end.  F_ONE (a reset sweep whose zeros were
+// written by K7 beforehand): the launch is one CTA and its only tile is init_tile.
+__device__ __forceinline__ uint64_t cta_tile(uint64_t j, const Params &P)
 {
-    return (uint64_t)blockIdx.x * NG + (j % NG) + (j / NG) * ((uint64_t)gridDim.x * NG);
+    if (P.flags & F_ONE) return j == 0 ? P.init_tile : ~0ull;
+    const uint64_t t = (uint64_t)blockIdx.x * NG + (j % NG) + (j / NG) * ((uint64_t)gridDim.x * NG);
+    return t < P.ntiles ? t : ~0ull;
 }
 
 // Hand buffer j % NBUF over to tile j (issued by the group that held it): load tile j into it, or
@@ -687,7 +690,7 @@ template <typename V>
 __device__ __forceinline__ void issue_tile(V *smbase, uint64_t *mbar, const V *psi, uint64_t j, uint64_t tbase,
                                            const Params &P, uint64_t gt, uint32_t tid, bool init)
 {
-    if (cta_tile(j) >= P.ntiles) return;
+    if (cta_tile(j, P) == ~0ull) return;
     const int b = (int)(j % NBUF);
     if (init) {
         mbar_arrive(&mbar[j % NMB]);
@@ -787,7 +790,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
     for (int b = 0; b < NTB; ++b) gt |= (uint64_t)((tid >> b) & 1u) << P.pin[b];
     // the first NBUF tiles: tile j is issued by group j % NG
     for (uint64_t j = grp; j < NBUF; j += NG)
-        issue_tile(smbase, mbar, src, j, pdep_outer(cta_tile(j), P.outer), P, gt, tid, init);
+        issue_tile(smbase, mbar, src, j, pdep_outer(cta_tile(j, P), P.outer), P, gt, tid, init);
     V a[NR];
     // thread parts of the phase-0 logical index (predicates, init) and of the last phase's write address
     uint64_t gthr0 = 0, gthr_st = 0;
@@ -800,26 +803,22 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         }
     }
     // read-layout tile base: the tile index deposited into the outer positions (stepped in place)
-    uint64_t base = pdep_outer(cta_tile(grp), P.outer);
+    uint64_t base = pdep_outer(cta_tile(grp, P), P.outer);
     const uint64_t dissue = P.dissue[grp];
     for (uint64_t j = grp;; j += NG, base = dep_add(base, P.dstep, P.outer)) {
-        const uint64_t T = cta_tile(j);
-        if (T >= P.ntiles) break;
+        const uint64_t T = cta_tile(j, P);
+        if (T == ~0ull) break;
         V *sm = smbase + (size_t)(j % NBUF) * (1u << TB);
         char *smb = reinterpret_cast<char *>(sm);
         const uint64_t bout = lookup(tabo, T);
         const uint64_t blog = need_l ? lookup(tabl, T) : 0;
         mbar_wait(&mbar[j % NMB], (uint32_t)((j / NMB) & 1));
-        // A reset sweep holds ONE nonzero element, in tile init_tile; the group's gates act inside
-        // tiles (outer qubits only as predicates), so every other tile is zero before and after
-        // them: those tiles skip the records and just store their zeros.
-        const bool zero_tile = init && T != P.init_tile;
         if (init) {
             // a reset: every amplitude is 0 but one, whose place in the phase-0 layout (after any
             // leading transposes, folded away on the host) the planner computed
 #pragma unroll
             for (int r = 0; r < NR; ++r) { a[r].x = R(0); a[r].y = R(0); }
-            if (!zero_tile && tid == P.init_t) {
+            if (tid == P.init_t) {   // (F_ONE: T is init_tile)
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
                     if ((uint32_t)r == P.init_r) { a[r].x = (R)P.init_re; a[r].y = (R)P.init_im; }
@@ -845,7 +844,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                 for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + (t0 ^ P.ph[0].so[r]));
             }
         }
-        if (P.last_xpose == 0xFFFFu || zero_tile) {   // no transpose in this group: release the buffer right away
+        if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: release the buffer right away
             if (P.flags & F_BULK) fence_proxy_async();
             named_bar(bar);
             issue_tile(smbase, mbar, src, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
@@ -860,9 +859,8 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         // -> branch chain was the top stall in ncu's source view; a shared-memory copy fetched by
         // a volatile load at the top of the iteration measured ~6 % slower)
         const uint64_t *recw = reinterpret_cast<const uint64_t *>(P.g);
-        const uint32_t ngate = zero_tile ? 0u : P.ngate;
-        uint64_t wnext = ngate ? recw[0] : 0;
-        for (uint32_t gi = 0; gi < ngate; ++gi) {
+        uint64_t wnext = P.ngate ? recw[0] : 0;
+        for (uint32_t gi = 0; gi < P.ngate; ++gi) {
             const uint64_t w = wnext;
             wnext = recw[gi + 1 < P.ngate ? gi + 1 : gi];
             GRec g;
@@ -2106,6 +2104,11 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         // LINEAR buffer; otherwise per-thread cp.async into the swizzled layout
         bool bulk = !pending_init;
         for (int b = 0; b < TB && bulk; ++b) bulk = P.pin[b] == b;
+        // ... read conflict-free from the linear buffer only when lanes 0-2 carry tile bits 0-2 (each
+        // quarter warp then reads one 128-byte row); a gather (leading transposes folded) reads
+        // arbitrary slots and keeps the swizzled staging (ncu: 7x bank conflicts from linear)
+        if (((1u << P.ph[0].tl[0]) | (1u << P.ph[0].tl[1]) | (1u << P.ph[0].tl[2])) != 7u) bulk = false;
+        if (P.ngate && P.g[0].code == C_XPOSE) bulk = false;
         {
             const Phase &f = P.ph[0], &l = P.ph[P.nphase - 1];
             P.regm_load = 0;
@@ -2303,6 +2306,17 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                     P.ph[k].so_out[r] = (uint16_t)(P.ph[k].so_out[r] * esz);
                 }
             if (ctx.timer) ctx.timer->begin(ctx.st);
+            if (pending_init) {
+                // A reset sweep: the group's gates act inside tiles, so every tile but init_tile stays
+                // zero.  K7 writes the zeros at streaming-store speed (any layout: zeros are zeros),
+                // then ONE CTA computes init_tile (F_ONE).  (Every tile computing its zeros in its
+                // own write layout measured 2.7-4.0 ms at n = 30; K7 alone is ~2.5 ms.)
+                launch_init_basis(dst, n_, prec_, 0, 0.0, 0.0, ctx.st);
+                if (want && cudaMemsetAsync(d_sums, 0, (size_t)P.ntiles * sizeof(double), ctx.st) != cudaSuccess)
+                    throw std::runtime_error("cudaMemsetAsync (block sums) failed");
+                P.flags |= F_ONE;
+                grid = 1;
+            }
             if (prec_ == 128)
                 k_fused<double><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((const double2 *)src, (double2 *)dst, P,
                                                                            d_sums);
@@ -2333,6 +2347,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
 #endif
         }
         count(ctx, bytes, true);
+        if (pending_init) ctx.stats->launches++;   // the K7 zero fill before the one-CTA sweep
         pending_init = false;
         xmask_ = P.xm_store ^ G.xa;
         if (want && sums_written) *sums_written = true;
