@@ -77,7 +77,8 @@ enum Code : uint16_t {
     C_CX2 = 123,  // +25c+5t1+t2 (t1 < t2): CX(c->t1) CX(c->t2) as ONE swap pass
     C_CU = 248,   // +6p+j   2x2 on bit p per pattern of the control pair j (Toffoli cores), 32 params
     C_CCX = 278,  // +6p+j   Toffoli on register bits: swap bit p where both controls of pair j are 1
-    C_TDK = 308,  // +r      bit 1 of reg r *= prod_k (pred(q_k) ? e^{i t_k} : 1), a = k count (3a params)
+    C_TDK = 308,  // +r      bit 1 of reg r *= prod_k (pred(q_k) ? e^{i t_k} : 1), a = k count: 2a params
+                  //         (q_k, t_k as a u64 turn fraction), or b = 1: 2 params (c, M), t_k = c << q_k
     C_N = 313,    // number of gate codes
     C_XPOSE = 313 // transpose registers to phase a
 };
@@ -484,34 +485,23 @@ __device__ __forceinline__ void gate_case(V (&a)[NR], const double *p, uint64_t 
         }
     } else if constexpr (C >= C_TDK) {
         // a run of controlled phases from outer/thread qubits onto one register bit (QFT ladders):
-        // the per-thread factor is a product of scalars, applied once.  Four independent partial
-        // products (k mod 4) cut the dependent complex-multiply chain (~30 links at 34 qubits) to
-        // a quarter; they are combined at the end.
-        double fr[4] = {1.0, 1.0, 1.0, 1.0}, fi[4] = {0.0, 0.0, 0.0, 0.0};
-        uint32_t k = 0;
-        for (; k + 4 <= ga; k += 4) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const double *e = p + 3 * (k + u);
-                if ((lbase >> (uint32_t)e[0]) & 1) {
-                    const double nr = fr[u] * e[1] - fi[u] * e[2];
-                    fi[u] = fr[u] * e[2] + fi[u] * e[1];
-                    fr[u] = nr;
-                }
-            }
+        // the per-thread factor is e^{2 pi i acc / 2^64}, acc = sum of the set predicates' angles
+        // as 64-bit turn fractions (integer adds, no chain of complex products), ONE sincospi.
+        // gb = 1 (geometric weights, a QFT ladder: angle_k = c * 2^{q_k} turns / 2^64):
+        // acc = (lbase & M) * c, a single multiply.
+        uint64_t acc = 0;
+        if (gb) {
+            acc = (lbase & (uint64_t)__double_as_longlong(p[1])) * (uint64_t)__double_as_longlong(p[0]);
+        } else {
+            for (uint32_t k = 0; k < ga; ++k)
+                if ((lbase >> (uint32_t)__double_as_longlong(p[2 * k])) & 1)
+                    acc += (uint64_t)__double_as_longlong(p[2 * k + 1]);
         }
-        for (; k < ga; ++k) {
-            const double *e = p + 3 * k;
-            if ((lbase >> (uint32_t)e[0]) & 1) {
-                const double nr = fr[0] * e[1] - fi[0] * e[2];
-                fi[0] = fr[0] * e[2] + fi[0] * e[1];
-                fr[0] = nr;
-            }
+        if (acc) {
+            double sn, cs;
+            sincospi((double)(long long)acc * 0x1p-63, &sn, &cs);
+            g_d1<C - C_TDK, V, R>(a, (R)cs, (R)sn);
         }
-        const double ar = fr[0] * fr[1] - fi[0] * fi[1], ai = fr[0] * fi[1] + fi[0] * fr[1];
-        const double br = fr[2] * fr[3] - fi[2] * fi[3], bi = fr[2] * fi[3] + fi[2] * fr[3];
-        const double tr = ar * br - ai * bi, ti = ar * bi + ai * br;
-        if (tr != 1.0 || ti != 0.0) g_d1<C - C_TDK, V, R>(a, (R)tr, (R)ti);
     } else if constexpr (C >= C_CCX) {
         constexpr int pb = (C - C_CCX) / 6;
         g_cx<(hdh_mask(pb, (C - C_CCX) % 6) & ~(1 << pb)), pb, V, true>(a);
@@ -1271,12 +1261,12 @@ namespace tq {
 static int rec_nparams(const GRec &r)
 {
     const uint16_t c = r.code;
-    if (c >= C_TDK && c < C_N) return 3 * r.a;
+    if (c >= C_TDK && c < C_N) return r.b ? 2 : 2 * r.a;
     if (c >= C_U && c < C_X) return 8;
     if (c >= C_D1 && c < C_D2) return 2;
     if (c >= C_D2 && c < C_CX) return 4;
     if (c >= C_CPH && c < C_TX) return 2;
-    if (c >= C_TD1 && c < C_TPH) return 2;
+    if (c >= C_TD1 && c < C_TPH) return 3;   // cos, sin, theta (theta for C_TDK merges)
     if (c == C_TPH) return 4;
     if (c >= C_DK && c < C_CX2) return 2 << __builtin_popcount(c - C_DK);
     if (c >= C_CU && c < C_CCX) return 32;
@@ -1637,7 +1627,7 @@ static void build_params(const Group &G, uint32_t n, Built &B, uint64_t tile, co
             } else if (a >= 0 || b >= 0) {
                 r.code = C_TD1 + (a >= 0 ? a : b);
                 r.a = (uint8_t)(a >= 0 ? o.q1 : o.q0);
-                r.pi = addp({pr, pi});
+                r.pi = addp({pr, pi, o.kind == CZ ? M_PI : o.theta});
             } else {
                 r.code = C_TPH;
                 r.a = (uint8_t)o.q0;
@@ -1712,12 +1702,36 @@ static void build_params(const Group &G, uint32_t n, Built &B, uint64_t tile, co
                 r.code = (uint16_t)(C_TDK + (c0 - C_TD1));
                 r.a = (uint8_t)(k - j);
                 r.pi = (uint16_t)prm.size();
+                // angles as 64-bit fractions of a turn (exact for the dyadic angles of a QFT)
+                std::vector<uint64_t> qk, ph;
                 for (size_t q = j; q < k; ++q) {
-                    const double e0 = (double)recs[q].a, e1 = prm[recs[q].pi], e2 = prm[recs[q].pi + 1];
-                    prm.push_back(e0);
-                    prm.push_back(e1);
-                    prm.push_back(e2);
+                    double f = prm[recs[q].pi + 2] / (2.0 * M_PI);
+                    f -= std::floor(f);
+                    const double w = std::ldexp(f, 64);
+                    qk.push_back(recs[q].a);
+                    ph.push_back(w >= 18446744073709551616.0 ? 0ull : (uint64_t)w);
                     newidx[q] = (uint16_t)m.size();
+                }
+                // geometric weights (angle_k = c << q_k mod 2^64, a QFT ladder): acc = (lbase & M) * c
+                size_t lo = 0;
+                for (size_t q = 1; q < qk.size(); ++q) if (qk[q] < qk[lo]) lo = q;
+                const uint64_t cgeo = ph[lo] >> qk[lo];
+                bool geo = (ph[lo] & ((1ull << qk[lo]) - 1)) == 0;
+                uint64_t mq = 0;
+                for (size_t q = 0; q < qk.size() && geo; ++q) {
+                    geo = (cgeo << qk[q]) == ph[q] && !(mq & bit(qk[q]));
+                    mq |= bit(qk[q]);
+                }
+                auto bits_of = [](uint64_t v) { double d; memcpy(&d, &v, 8); return d; };
+                if (geo) {
+                    r.b = 1;
+                    prm.push_back(bits_of(cgeo));
+                    prm.push_back(bits_of(mq));
+                } else {
+                    for (size_t q = 0; q < qk.size(); ++q) {
+                        prm.push_back(bits_of(qk[q]));
+                        prm.push_back(bits_of(ph[q]));
+                    }
                 }
                 m.push_back(r);
                 j = k - 1;
