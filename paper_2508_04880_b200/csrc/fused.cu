@@ -79,8 +79,11 @@ enum Code : uint16_t {
     C_CCX = 278,  // +6p+j   Toffoli on register bits: swap bit p where both controls of pair j are 1
     C_TDK = 308,  // +r      bit 1 of reg r *= prod_k (pred(q_k) ? e^{i t_k} : 1), a = k count: 2a params
                   //         (q_k, t_k as a u64 turn fraction), or b = 1: 2 params (c, M), t_k = c << q_k
-    C_N = 313,    // number of gate codes
-    C_XPOSE = 313 // transpose registers to phase a
+    C_DKC = 313,  // +16t+m  bit t of r set: a[r] *= tab[pext(r, M)], M = the 4-bit m spread over the
+                  //         register bits other than t (2 * 2^popc(m) params): a diagonal table whose
+                  //         entries with bit t clear are 1 (a CP ladder onto t), half the multiplies
+    C_N = 393,    // number of gate codes
+    C_XPOSE = 393 // transpose registers to phase a
 };
 
 // the j-th (0..5) pair {u < v} of register bits other than p, as a mask (with p): the diagonal of a
@@ -95,6 +98,18 @@ __host__ __device__ constexpr int hdh_mask(int p, int j)
             ++k;
         }
     return 0;
+}
+
+// m (4 bits) spread over the 5 register bits other than t
+__host__ __device__ constexpr int spread_skip(int m, int t)
+{
+    int o = 0, k = 0;
+    for (int b = 0; b < 5; ++b) {
+        if (b == t) continue;
+        if ((m >> k) & 1) o |= 1 << b;
+        ++k;
+    }
+    return o;
 }
 
 __host__ __device__ constexpr int pext5(int r, int m)
@@ -357,6 +372,18 @@ __device__ __forceinline__ void g_dk(V (&a)[NR], const double *tab)
     for (int i = 0; i < NR; ++i) cmul_ip(a[i], tr[pext5(i, M)], ti[pext5(i, M)]);
 }
 
+template <int T, int M, typename V, typename R>
+__device__ __forceinline__ void g_dkc(V (&a)[NR], const double *tab)
+{
+    constexpr int K = __builtin_popcount(M);
+    R tr[1 << K], ti[1 << K];
+#pragma unroll
+    for (int idx = 0; idx < (1 << K); ++idx) { tr[idx] = (R)tab[2 * idx]; ti[idx] = (R)tab[2 * idx + 1]; }
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+        if ((i >> T) & 1) cmul_ip(a[i], tr[pext5(i, M)], ti[pext5(i, M)]);
+}
+
 // new (x, y) = (m00 x + m01 y, m10 x + m11 y), in place
 __device__ __forceinline__ void mat2_ip(double2 &x, double2 &y, const double *m)
 {
@@ -442,6 +469,7 @@ __host__ __device__ constexpr bool code_ok(int C)
     if (C < C_TPH) return (C - C_TX) % 5 < RB;
     if (C == C_TPH) return true;
     if (C < C_CX2) return C - C_DK < NR;
+    if (C >= C_DKC) return (C - C_DKC) / 16 < RB;
     if (C >= C_TDK) return (C - C_TDK) < RB;
     if (C >= C_CCX) return hdh_mask((C - C_CCX) / 6, (C - C_CCX) % 6) < NR;
     if (C >= C_CU) return hdh_mask((C - C_CU) / 6, (C - C_CU) % 6) < NR;
@@ -483,6 +511,9 @@ __device__ __forceinline__ void gate_case(V (&a)[NR], const double *p, uint64_t 
 #pragma unroll
             for (int i = 0; i < NR; ++i) cmul_ip(a[i], fr, fi);
         }
+    } else if constexpr (C >= C_DKC) {
+        constexpr int t = (C - C_DKC) / 16;
+        if constexpr (t < RB) g_dkc<t, spread_skip((C - C_DKC) % 16, t), V, R>(a, p);
     } else if constexpr (C >= C_TDK) {
         // a run of controlled phases from outer/thread qubits onto one register bit (QFT ladders):
         // the per-thread factor is e^{2 pi i acc / 2^64}, acc = sum of the set predicates' angles
@@ -535,7 +566,8 @@ __device__ __forceinline__ void apply_gate(V (&a)[NR], const GRec &g, const doub
     // fast paths for the two hottest classes (H and diagonal tables: ~2/3 of all records)
     // ordered by frequency in Adder groups: Toffoli swaps, CX, diagonal tables, H, CU, rest
     const int c = g.code;
-    if (c >= C_TDK) dispatch<C_TDK, C_N, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    if (c >= C_DKC) dispatch<C_DKC, C_N, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
+    else if (c >= C_TDK) dispatch<C_TDK, C_DKC, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
     else if (c >= C_CCX) dispatch<C_CCX, C_TDK, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
     else if (c >= C_CX && c < C_CPH) dispatch<C_CX, C_CPH, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
     else if (c >= C_DK && c < C_DK + NR) dispatch<C_DK, C_DK + NR, V, R>(c, a, prm + g.pi, lbase, g.a, g.b);
@@ -1261,7 +1293,8 @@ namespace tq {
 static int rec_nparams(const GRec &r)
 {
     const uint16_t c = r.code;
-    if (c >= C_TDK && c < C_N) return r.b ? 2 : 2 * r.a;
+    if (c >= C_DKC && c < C_N) return 2 << __builtin_popcount((c - C_DKC) % 16);
+    if (c >= C_TDK && c < C_DKC) return r.b ? 2 : 2 * r.a;
     if (c >= C_U && c < C_X) return 8;
     if (c >= C_D1 && c < C_D2) return 2;
     if (c >= C_D2 && c < C_CX) return 4;
@@ -1900,6 +1933,34 @@ static void build_params(const Group &G, uint32_t n, Built &B, uint64_t tile, co
         }
         recs.swap(kept);
     }
+    // Diagonal tables whose entries with some register bit t clear are exactly 1 (a CP ladder onto
+    // t: the QFT's in-register phases) become controlled tables: half the multiplies and loads.
+    for (auto &r : recs) {
+        if (r.code < C_DK || r.code >= C_DK + NR) continue;
+        const int M = r.code - C_DK, K = __builtin_popcount((unsigned)M);
+        const double *tab = prm.data() + r.pi;
+        for (int t = 0; t < RB; ++t) {
+            if (!((M >> t) & 1)) continue;
+            const int kt = __builtin_popcount((unsigned)(M & ((1 << t) - 1)));   // t's index in the pext
+            bool ctl = true;
+            for (int e = 0; e < (1 << K) && ctl; ++e)
+                if (!((e >> kt) & 1)) ctl = tab[2 * e] == 1.0 && tab[2 * e + 1] == 0.0;
+            if (!ctl) continue;
+            int m4 = 0, k = 0;   // the other bits of M, numbered over the register bits other than t
+            for (int b = 0; b < RB; ++b) {
+                if (b == t) continue;
+                if ((M >> b) & 1) m4 |= 1 << k;
+                ++k;
+            }
+            std::vector<double> sub;
+            for (int e = 0; e < (1 << K); ++e)
+                if ((e >> kt) & 1) { sub.push_back(tab[2 * e]); sub.push_back(tab[2 * e + 1]); }
+            r.code = (uint16_t)(C_DKC + 16 * t + m4);
+            r.pi = (uint16_t)prm.size();
+            prm.insert(prm.end(), sub.begin(), sub.end());
+            break;
+        }
+    }
     {   // compact the parameter block (merges leave their inputs' parameters unused)
         std::vector<double> used;
         used.reserve(prm.size());
@@ -2265,7 +2326,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         P.flags = 0;
         for (uint32_t i = 0; i < P.ngate; ++i) {   // records that read the logical index
             const uint16_t c = P.g[i].code;
-            if ((c >= C_TX && c <= C_TPH) || (c >= C_TDK && c < C_N)) P.flags |= F_LBASE;
+            if ((c >= C_TX && c <= C_TPH) || (c >= C_TDK && c < C_DKC)) P.flags |= F_LBASE;
         }
         if (bulk) P.flags |= F_BULK;
         if (pending_init) {
@@ -2344,10 +2405,10 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 int cnt[10] = {0};   // H, DK, CX-like, D, XPOSE, XY, T-pred, other, CU, CCX
                 for (uint32_t i = 0; i < P.ngate; ++i) {
                     const uint16_t c = P.g[i].code;
-                    const int k = c < C_U ? 0 : (c >= C_DK && c < C_CX2) ? 1
+                    const int k = c < C_U ? 0 : ((c >= C_DK && c < C_CX2) || (c >= C_DKC && c < C_N)) ? 1
                                 : ((c >= C_CX && c < C_CPH) || (c >= C_CX2 && c < C_CU)) ? 2
                                 : (c >= C_D1 && c < C_CX) ? 3 : c == C_XPOSE ? 4 : (c >= C_X && c < C_D1) ? 5
-                                : ((c >= C_TX && c <= C_TPH) || (c >= C_TDK && c < C_N)) ? 6
+                                : ((c >= C_TX && c <= C_TPH) || (c >= C_TDK && c < C_DKC)) ? 6
                                 : (c >= C_CU && c < C_CCX) ? 8 : (c >= C_CCX && c < C_TDK) ? 9 : 7;
                     cnt[k]++;
                 }
