@@ -136,7 +136,7 @@ struct GRec {
     uint16_t _pad;
 };
 
-enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8, F_BULK = 16, F_ONE = 32 };
+enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8, F_BULK = 16, F_LIVE = 32 };
 constexpr int NCH = 4;             // 8-bit chunks of the tile index (n <= TB + 8 * NCH = 44 fused)
 
 // Qubit layout: the state may be stored with its qubits permuted (logical qubit q at physical bit
@@ -148,8 +148,10 @@ constexpr int NCH = 4;             // 8-bit chunks of the tile index (n <= TB + 
 struct Params {
     uint64_t xm_load, xm_store;   // logical X-relabel mask at load / at store (outer bits only)
     uint64_t xin, xout;           // xm_store in the read / write layout
-    uint64_t init_tile;           // F_INIT: the state is init_re + i init_im at ONE element: register
-    uint32_t init_t, init_r;      //   init_r of thread init_t of tile init_tile (phase-0 layout), 0 elsewhere
+    uint32_t init_t, init_r;      // F_INIT: the state is init_re + i init_im at ONE element: register
+                                  //   init_r of thread init_t of the (single, F_LIVE) tile, 0 elsewhere
+    uint64_t lfree, lfix;         // F_LIVE: only the tiles T = pdep(i, lfree) | lfix, i < nlive, can hold
+    uint64_t nlive;               //   nonzero amplitudes (support analysis); the rest stay zero
     double init_re, init_im;
     double scale_re, scale_im;
     uint64_t ntiles;
@@ -697,12 +699,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t parity)
                  : "memory");
 }
 
-// tile index of this CTA's j-th tile, or ~0 past the end.  F_ONE (a reset sweep whose zeros were
-// written by K7 beforehand): the launch is one CTA and its only tile is init_tile.
+__device__ __forceinline__ uint64_t pdep64(uint64_t x, uint64_t m)
+{
+    uint64_t o = 0;
+    for (; m && x; m &= m - 1, x >>= 1)
+        if (x & 1) o |= m & (~m + 1);
+    return o;
+}
+
+// tile index of this CTA's j-th tile, or ~0 past the end.  F_LIVE (a sweep right after a reset,
+// DESIGN.md "Live tiles"): only the nlive tiles the support analysis allows are visited; the
+// others hold zeros (K7 wrote them) and the group's gates keep them zero.
 __device__ __forceinline__ uint64_t cta_tile(uint64_t j, const Params &P)
 {
-    if (P.flags & F_ONE) return j == 0 ? P.init_tile : ~0ull;
     const uint64_t t = (uint64_t)blockIdx.x * NG + (j % NG) + (j / NG) * ((uint64_t)gridDim.x * NG);
+    if (P.flags & F_LIVE) return t < P.nlive ? pdep64(t, P.lfree) | P.lfix : ~0ull;
     return t < P.ntiles ? t : ~0ull;
 }
 
@@ -830,6 +841,9 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
     for (uint64_t j = grp;; j += NG, base = dep_add(base, P.dstep, P.outer)) {
         const uint64_t T = cta_tile(j, P);
         if (T == ~0ull) break;
+        const bool live = P.flags & F_LIVE;
+        if (live) base = pdep_outer(T, P.outer);   // sparse tile sequence: no incremental bases
+        const uint64_t nbase = live ? pdep_outer(cta_tile(j + NBUF, P), P.outer) : dep_add(base, dissue, P.outer);
         V *sm = smbase + (size_t)(j % NBUF) * (1u << TB);
         char *smb = reinterpret_cast<char *>(sm);
         const uint64_t bout = lookup(tabo, T);
@@ -840,7 +854,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
             // leading transposes, folded away on the host) the planner computed
 #pragma unroll
             for (int r = 0; r < NR; ++r) { a[r].x = R(0); a[r].y = R(0); }
-            if (tid == P.init_t) {   // (F_ONE: T is init_tile)
+            if (tid == P.init_t) {   // (F_INIT comes with F_LIVE: T is the one live tile)
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
                     if ((uint32_t)r == P.init_r) { a[r].x = (R)P.init_re; a[r].y = (R)P.init_im; }
@@ -869,7 +883,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: release the buffer right away
             if (P.flags & F_BULK) fence_proxy_async();
             named_bar(bar);
-            issue_tile(smbase, mbar, src, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
+            issue_tile(smbase, mbar, src, j + NBUF, nbase, P, gt, tid, init);
         }
 
         // ONE flat loop over records; a phase change is just a record (C_XPOSE) so that all paths
@@ -931,7 +945,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                 if (gi == P.last_xpose) {   // the buffer is free until tile j + NBUF: hand it over
                     if (P.flags & F_BULK) fence_proxy_async();
                     named_bar(bar);
-                    issue_tile(smbase, mbar, src, j + NBUF, dep_add(base, dissue, P.outer), P, gt, tid, init);
+                    issue_tile(smbase, mbar, src, j + NBUF, nbase, P, gt, tid, init);
                 }
             }
         }
@@ -2112,6 +2126,45 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     // number of layout-changing sweeps must be even for the state to end in ctx.psi: with an odd
     // number of groups, boundary 1 keeps the identity (group 0 runs in place).  Without a second
     // buffer every layout is the identity and every sweep runs in place.
+    // ---- live tiles.  After a reset the state is ONE basis state; a gate
+    // can only make a qubit vary if it is an exchange gate on it (H, RX, RY, U) or a CX whose
+    // control already varies; X / Y / CX with a fixed control just flip a fixed bit; diagonals
+    // change nothing.  So before launched group k the nonzero amplitudes lie in {x : x_q = b_q
+    // for q outside S_k}, and group k only has to visit the 2^|S_k \ tile_k| tiles with those
+    // outer bits -- the others are zero (K7 wrote them) and stay zero (the group's gates act
+    // inside tiles).  The leading groups whose live tiles are <= 1/8 of all run IN PLACE in the
+    // identity layout over their live tiles only (F_LIVE); the first reset group is one tile.
+    std::vector<uint64_t> supS(NLG, ~0ull), supB(NLG, 0);
+    size_t KP = 0;
+    if (pending_init) {
+        uint64_t sup = 0, bx = init->index;   // qubits that may vary; values of the others
+        auto step = [&](const Op &o) {
+            const uint64_t b0 = bit(o.q0), b1 = two_qubit(o.kind) ? bit(o.q1) : 0;
+            switch (o.kind) {
+            case Kind::I: case Kind::Z: case Kind::S: case Kind::SDG: case Kind::T: case Kind::TDG:
+            case Kind::P: case Kind::RZ: case Kind::CZ: case Kind::CP: break;
+            case Kind::X: case Kind::Y: if (!(sup & b0)) bx ^= b0; break;
+            case Kind::CX:
+                if (sup & b0) sup |= b1;
+                else if ((bx & b0) && !(sup & b1)) bx ^= b1;
+                break;
+            default: sup |= b0 | b1; break;   // H, RX, RY and anything else: the qubits may vary
+            }
+        };
+        bool pi = true;
+        size_t k = 0;
+        for (const Group &G : groups) {
+            const bool launch = !G.ops.empty() || pi;
+            pi = false;
+            bx ^= G.xb & ~sup;
+            if (launch) { supS[k] = sup; supB[k] = bx; ++k; }
+            for (const KOp &ko : G.ops) step(ko.op);
+            bx ^= G.xa & ~sup;
+        }
+        const uint64_t all = n_ >= 64 ? ~0ull : (1ull << n_) - 1;
+        while (KP < NLG && __builtin_popcountll(supS[KP] & ~tiles[KP] & all) + 3 <= (int)(n_ - TB)) ++KP;
+        if (KP == 0) KP = 1;   // the reset group itself is always one tile
+    }
     std::vector<std::array<uint8_t, 64>> lay(NLG + 1);
 #ifdef TUSQ_DEBUG_KNOBS   // debug builds only: TUSQ_DBG_IDENTITY=1 keeps every layout the identity
     static const bool dbg_identity = getenv("TUSQ_DBG_IDENTITY") != nullptr;
@@ -2125,7 +2178,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     const bool remap = alt_ != nullptr && !dbg_identity && NLG >= 2;
     for (size_t k = 0; k <= NLG; ++k) {
         auto &L = lay[k];
-        if (k == 0 || k == NLG || !remap) {
+        if (k <= KP || k == NLG || !remap) {   // (live-tile sweeps run in place: identity)
             for (uint32_t q = 0; q < 64; ++q) L[q] = (uint8_t)q;
             continue;
         }
@@ -2166,6 +2219,8 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         // loads go through shared memory (always coalesced): no load-layout phase needed
         build_params(G, n_, B, tiles[lk], lay[lk].data(), lay[lk + 1].data());
         Params &P = B.P;
+        const size_t kq = lk;          // this group's launch index (lk advances below)
+        uint64_t init_tile = 0;        // the reset group's one tile (tile-index bits)
         void *src = cur;
         void *dst = lay[lk] == lay[lk + 1] ? cur : (cur == ctx.psi ? alt_ : ctx.psi);
         cur = dst;
@@ -2232,6 +2287,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             // ladders of an Adder group) fold into the first shared-memory read: the data movement of
             // the whole chain is simulated here and the read becomes a gather through a table
             P.gtab = 0xFFFFu;
+            init_tile = 0;
             uint32_t kstar = 0;
             while (kstar < P.ngate && P.g[kstar].code == C_XPOSE) ++kstar;
             // A reset group holds ONE nonzero element: its leading transposes fold away entirely
@@ -2261,8 +2317,8 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 const uint64_t lstar = init->index ^ m_load;
                 uint32_t estar = 0;
                 for (int b = 0; b < TB; ++b) estar |= (uint32_t)((lstar >> P.qs[b]) & 1u) << b;
-                P.init_tile = 0;
-                for (uint32_t k = 0; k < P.nout; ++k) P.init_tile |= ((lstar >> P.ol[k]) & 1ull) << k;
+                init_tile = 0;
+                for (uint32_t k = 0; k < P.nout; ++k) init_tile |= ((lstar >> P.ol[k]) & 1ull) << k;
                 const uint16_t want = (uint16_t)swz(estar);
                 bool found = false;
                 for (uint32_t t = 0; t < (uint32_t)NT && !found; ++t)
@@ -2334,6 +2390,21 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             P.init_re = init->re;
             P.init_im = init->im;
         }
+        if (kq < KP) {   // live-tile sweep (in place, identity layout)
+            P.flags |= F_LIVE;
+            P.lfree = P.lfix = 0;
+            if (pending_init) {
+                P.lfix = init_tile;
+            } else {
+                for (uint32_t j = 0; j < P.nout; ++j) {
+                    const uint32_t q = P.ol[j];
+                    if (supS[kq] & bit(q)) P.lfree |= 1ull << j;
+                    else P.lfix |= ((supB[kq] >> q) & 1ull) << j;
+                }
+            }
+            P.nlive = 1ull << __builtin_popcountll(P.lfree);
+        }
+        const double tbytes = (double)(1u << TB) * (prec_ == 128 ? 16 : 8);
         double sc = 1.0;
         int nh = 0;
         for (auto &k : G.ops) nh += k.op.kind == H;
@@ -2346,10 +2417,11 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         const bool last = gi + 1 == groups.size();
         bool want = last && d_sums && B.tile == ((1ull << TB) - 1);
         if (want) P.flags |= F_SUMS;
-        const double bytes = pending_init ? s : 2 * s;
+        const double bytes = pending_init ? s : (P.flags & F_LIVE) ? 2.0 * (double)P.nlive * tbytes : 2 * s;
         if (!ctx.dry) {
             int bps = blocks_per_sm(prec_);
-            uint64_t grid = std::min<uint64_t>((P.ntiles + NG - 1) / NG, (uint64_t)device_sm_count() * bps);
+            const uint64_t nt = (P.flags & F_LIVE) ? P.nlive : P.ntiles;
+            uint64_t grid = std::min<uint64_t>((nt + NG - 1) / NG, (uint64_t)device_sm_count() * bps);
 #ifdef TUSQ_DEBUG_KNOBS   // TUSQ_DBG_GRID=g caps the grid (several tiles per CTA at small n)
             static const uint64_t dbg_grid = getenv("TUSQ_DBG_GRID") ? (uint64_t)atoll(getenv("TUSQ_DBG_GRID")) : 0;
             if (dbg_grid) grid = std::min(grid, dbg_grid);
@@ -2382,16 +2454,16 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 }
             if (ctx.timer) ctx.timer->begin(ctx.st);
             if (pending_init) {
-                // A reset sweep: the group's gates act inside tiles, so every tile but init_tile stays
-                // zero.  K7 writes the zeros at streaming-store speed (any layout: zeros are zeros),
-                // then ONE CTA computes init_tile (F_ONE).  (Every tile computing its zeros in its
+                // A reset sweep: the group's gates act inside tiles, so every tile but the one holding
+                // the basis state stays zero.  K7 writes the zeros at streaming-store speed, then ONE
+                // CTA computes that tile (F_LIVE, nlive = 1).  (Every tile computing its zeros in its
                 // own write layout measured 2.7-4.0 ms at n = 30; K7 alone is ~2.5 ms.)
                 launch_init_basis(dst, n_, prec_, 0, 0.0, 0.0, ctx.st);
-                if (want && cudaMemsetAsync(d_sums, 0, (size_t)P.ntiles * sizeof(double), ctx.st) != cudaSuccess)
-                    throw std::runtime_error("cudaMemsetAsync (block sums) failed");
-                P.flags |= F_ONE;
-                grid = 1;
             }
+            // live-tile sweeps write the sums of their live tiles only: the others are zero
+            if ((P.flags & F_LIVE) && want &&
+                cudaMemsetAsync(d_sums, 0, (size_t)P.ntiles * sizeof(double), ctx.st) != cudaSuccess)
+                throw std::runtime_error("cudaMemsetAsync (block sums) failed");
             if (prec_ == 128)
                 k_fused<double><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((const double2 *)src, (double2 *)dst, P,
                                                                            d_sums);
