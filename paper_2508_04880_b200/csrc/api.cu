@@ -556,7 +556,7 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
             if (!dry) launch_init_basis(psi, n, prec, vstate.index, vstate.re, vstate.im, st);
             stats.launches++;
             stats.hbm_bytes += (double)need;
-            if (fuse) planner.reset_mask();
+            if (fuse) planner.note_basis(vstate.index);
         }
         if (fuse) planner.materialize(ctx);   // leave the caller's buffer in logical order
         if (!dry && !fills.empty()) {   // the virtual leaves' draws, one launch

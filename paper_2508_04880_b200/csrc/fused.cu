@@ -2093,7 +2093,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     if (groups.empty() && pending_init) {
         if (!ctx.dry) launch_init_basis(ctx.psi, n_, prec_, init->index, init->re, init->im, ctx.st);
         count(ctx, s, false);
-        xmask_ = 0;
+        note_basis(init->index);
         return true;
     }
     if (!scratch_) scratch_ = std::make_shared<PlanScratch>();
@@ -2134,10 +2134,16 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     // outer bits -- the others are zero (K7 wrote them) and stay zero (the group's gates act
     // inside tiles).  The leading groups whose live tiles are <= 1/8 of all run IN PLACE in the
     // identity layout over their live tiles only (F_LIVE); the first reset group is one tile.
+    // Without a reset the analysis continues from the support known after the previous call
+    // (dfree_ / dfix_: physical, identity layout; logical = physical ^ xmask_).
+    const uint64_t all = n_ >= 64 ? ~0ull : (1ull << n_) - 1;
     std::vector<uint64_t> supS(NLG, ~0ull), supB(NLG, 0);
     size_t KP = 0;
-    if (pending_init) {
-        uint64_t sup = 0, bx = init->index;   // qubits that may vary; values of the others
+    const bool track = pending_init || (dfree_ & all) != all;
+    uint64_t sup_end = all, bx_end = 0;
+    if (track) {
+        uint64_t sup = pending_init ? 0 : dfree_ & all;   // qubits that may vary
+        uint64_t bx = pending_init ? init->index : (dfix_ ^ xmask_) & ~sup;   // values of the others
         auto step = [&](const Op &o) {
             const uint64_t b0 = bit(o.q0), b1 = two_qubit(o.kind) ? bit(o.q1) : 0;
             switch (o.kind) {
@@ -2161,10 +2167,13 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             for (const KOp &ko : G.ops) step(ko.op);
             bx ^= G.xa & ~sup;
         }
-        const uint64_t all = n_ >= 64 ? ~0ull : (1ull << n_) - 1;
+        sup_end = sup;
+        bx_end = bx;
         while (KP < NLG && __builtin_popcountll(supS[KP] & ~tiles[KP] & all) + 3 <= (int)(n_ - TB)) ++KP;
-        if (KP == 0) KP = 1;   // the reset group itself is always one tile
+        if (KP == 0 && pending_init && NLG) KP = 1;   // the reset group itself is always one tile
     }
+    // the part of the buffer a reset must zero: what the previous call may have left nonzero
+    const uint64_t zfree = dfree_ & all, zfix = dfix_ & all & ~zfree;
     std::vector<std::array<uint8_t, 64>> lay(NLG + 1);
 #ifdef TUSQ_DEBUG_KNOBS   // debug builds only: TUSQ_DBG_IDENTITY=1 keeps every layout the identity
     static const bool dbg_identity = getenv("TUSQ_DBG_IDENTITY") != nullptr;
@@ -2417,7 +2426,9 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         const bool last = gi + 1 == groups.size();
         bool want = last && d_sums && B.tile == ((1ull << TB) - 1);
         if (want) P.flags |= F_SUMS;
-        const double bytes = pending_init ? s : (P.flags & F_LIVE) ? 2.0 * (double)P.nlive * tbytes : 2 * s;
+        const double zbytes = __builtin_popcountll(zfree) + 2 <= (int)n_
+                                  ? (double)(1ull << __builtin_popcountll(zfree)) * (prec_ == 128 ? 16 : 8) : s;
+        const double bytes = pending_init ? zbytes : (P.flags & F_LIVE) ? 2.0 * (double)P.nlive * tbytes : 2 * s;
         if (!ctx.dry) {
             int bps = blocks_per_sm(prec_);
             const uint64_t nt = (P.flags & F_LIVE) ? P.nlive : P.ntiles;
@@ -2458,7 +2469,8 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 // the basis state stays zero.  K7 writes the zeros at streaming-store speed, then ONE
                 // CTA computes that tile (F_LIVE, nlive = 1).  (Every tile computing its zeros in its
                 // own write layout measured 2.7-4.0 ms at n = 30; K7 alone is ~2.5 ms.)
-                launch_init_basis(dst, n_, prec_, 0, 0.0, 0.0, ctx.st);
+                if (__builtin_popcountll(zfree) + 2 <= (int)n_) launch_zero_affine(dst, n_, prec_, zfree, zfix, ctx.st);
+                else launch_init_basis(dst, n_, prec_, 0, 0.0, 0.0, ctx.st);
             }
             // live-tile sweeps write the sums of their live tiles only: the others are zero
             if ((P.flags & F_LIVE) && want &&
@@ -2500,12 +2512,21 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         if (want && sums_written) *sums_written = true;
     }
     if (cur != ctx.psi) throw std::runtime_error("fused planner: layout parity left the state in the scratch buffer");
+    // what the buffer may hold from now on: the final support if every sweep was a live one
+    if (track && KP == NLG) {
+        dfree_ = sup_end;
+        dfix_ = (bx_end ^ xmask_) & ~sup_end & all;
+    } else {
+        dfree_ = ~0ull;
+        dfix_ = 0;
+    }
     return true;
 }
 
 void FusedPlanner::materialize(Ctx &ctx)
 {
     if (!xmask_) return;
+    dfix_ ^= xmask_ & ~dfree_;   // the XOR moves the known support with the state
     double b = 0;
     if (!ctx.dry) b = launch_pauli_string(ctx.psi, n_, prec_, xmask_, 0, ctx.st);
     else b = 2.0 * (double)(1ull << n_) * (prec_ == 128 ? 16 : 8);

@@ -76,6 +76,8 @@ public:
     }
     void materialize(Ctx &ctx);
     void reset_mask() { xmask_ = 0; }
+    // the caller wrote the basis state |index> (K7) into the state: the known support is one element
+    void note_basis(uint64_t index) { xmask_ = 0; dfree_ = 0; dfix_ = index; }
 
 private:
     uint32_t n_;
@@ -83,6 +85,9 @@ private:
     uint32_t tile_bits_;
     bool enabled_;
     uint64_t xmask_ = 0;
+    // known support of the state in ctx.psi (physical positions, identity layout): every nonzero
+    // amplitude has (index & ~dfree_) == dfix_; dfree_ = ~0 when unknown
+    uint64_t dfree_ = ~0ull, dfix_ = 0;
     void *alt_ = nullptr;
     uint64_t alt_lazy_ = 0;
     bool alt_owned_ = false;

@@ -328,6 +328,36 @@ double launch_pauli_string(void *psi, uint32_t n, int prec, uint64_t xm, uint64_
     return prec == 64 ? pauli_impl<float>(psi, n, xm, zm, st) : pauli_impl<double>(psi, n, xm, zm, st);
 }
 
+// zeros at every index x with (x & ~free) == fix: the part of a state that may be nonzero when a
+// support analysis bounds it (K5 live tiles), written before a reset instead of the whole state
+template <typename V>
+__global__ void __launch_bounds__(TPB) k_zero_affine(V *__restrict__ psi, uint64_t cnt, uint64_t free, uint64_t fix)
+{
+    for (uint64_t i = (uint64_t)blockIdx.x * TPB + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * TPB) {
+        uint64_t o = fix, x = i;
+        for (uint64_t m = free; m && x; m &= m - 1, x >>= 1)
+            if (x & 1) o |= m & (~m + 1);
+        V z;
+        z.x = 0;
+        z.y = 0;
+        psi[o] = z;
+    }
+}
+
+double launch_zero_affine(void *psi, uint32_t n, int prec, uint64_t free, uint64_t fix, cudaStream_t st)
+{
+    const uint64_t all = n >= 64 ? ~0ull : (1ull << n) - 1;
+    free &= all;
+    fix &= all & ~free;
+    const uint64_t cnt = 1ull << __builtin_popcountll(free);
+    if (prec == 64) {
+        k_zero_affine<float2><<<grid_for(cnt, TPB, 1), TPB, 0, st>>>((float2 *)psi, cnt, free, fix);
+        return cnt * 8.0;
+    }
+    k_zero_affine<double2><<<grid_for(cnt, TPB, 1), TPB, 0, st>>>((double2 *)psi, cnt, free, fix);
+    return cnt * 16.0;
+}
+
 double launch_init_basis(void *psi, uint32_t n, int prec, uint64_t index, double re, double im, cudaStream_t st)
 {
     const uint64_t N = 1ull << n;

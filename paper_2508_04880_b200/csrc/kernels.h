@@ -13,6 +13,8 @@ double launch_gate(void *psi, uint32_t n, int prec, const Op &op, cudaStream_t s
 double launch_pauli_string(void *psi, uint32_t n, int prec, uint64_t xmask, uint64_t zmask, cudaStream_t st);
 // K7: psi <- amp |index>
 double launch_init_basis(void *psi, uint32_t n, int prec, uint64_t index, double re, double im, cudaStream_t st);
+// zeros on the affine set {x : (x & ~free) == fix} (the part a support analysis says may be nonzero)
+double launch_zero_affine(void *psi, uint32_t n, int prec, uint64_t free, uint64_t fix, cudaStream_t st);
 
 // ----- K6: sampler ---------------------------------------------------------------------
 // block sums of |amp|^2 over contiguous blocks of 2^block_bits amplitudes
