@@ -523,7 +523,12 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
                 const uint64_t xm = fuse ? planner.xmask() : 0;
                 if (ctx.timer) ctx.timer->begin(st);
                 if (!phys_sums_valid) {
-                    stats.sample_bytes += dry ? (double)need : launch_block_sums(psi, n, prec, bb, d_blocks, st);
+                    uint64_t vf = ~0ull, vx = 0;   // K5 live tiles may leave the buffer valid on a subset
+                    if (fuse) {
+                        planner.close_blocks(ctx, bb);
+                        planner.valid_set(&vf, &vx);
+                    }
+                    stats.sample_bytes += dry ? (double)need : launch_block_sums(psi, n, prec, bb, d_blocks, st, vf, vx);
                     stats.launches++;
                     phys_sums_valid = true;
                 }
@@ -558,7 +563,10 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
             stats.hbm_bytes += (double)need;
             if (fuse) planner.note_basis(vstate.index);
         }
-        if (fuse) planner.materialize(ctx);   // leave the caller's buffer in logical order
+        if (fuse) {   // leave the caller's buffer in logical order, whole
+            planner.materialize(ctx);
+            planner.finish(ctx);
+        }
         if (!dry && !fills.empty()) {   // the virtual leaves' draws, one launch
             void *fb = nullptr;
             TQ_RUN_CUDA(scratch_alloc(&fb, fills.size() * 8, st));

@@ -136,7 +136,7 @@ struct GRec {
     uint16_t _pad;
 };
 
-enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8, F_BULK = 16, F_LIVE = 32 };
+enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8, F_BULK = 16, F_LIVE = 32, F_VMASK = 64 };
 constexpr int NCH = 4;             // 8-bit chunks of the tile index (n <= TB + 8 * NCH = 44 fused)
 
 // Qubit layout: the state may be stored with its qubits permuted (logical qubit q at physical bit
@@ -152,6 +152,10 @@ struct Params {
                                   //   init_r of thread init_t of the (single, F_LIVE) tile, 0 elsewhere
     uint64_t lfree, lfix;         // F_LIVE: only the tiles T = pdep(i, lfree) | lfix, i < nlive, can hold
     uint64_t nlive;               //   nonzero amplitudes (support analysis); the rest stay zero
+    uint64_t vfree, vfix;         // F_VMASK (read layout = identity): the buffer holds the state only on
+                                  //   {x : (x & ~vfree) == vfix}; elsewhere it is zero but not written:
+                                  //   tiles outside are not loaded (zeros), elements outside read as 0
+    uint32_t vl_mask, vl_val;     //   the same condition on the tile-local bits
     double init_re, init_im;
     double scale_re, scale_im;
     uint64_t ntiles;
@@ -717,6 +721,12 @@ __device__ __forceinline__ uint64_t cta_tile(uint64_t j, const Params &P)
     return t < P.ntiles ? t : ~0ull;
 }
 
+// F_VMASK: a tile (read-layout base tbase) none of whose elements the buffer holds: it is all zero
+__device__ __forceinline__ bool tile_dead(uint64_t tbase, const Params &P)
+{
+    return (P.flags & F_VMASK) && (((tbase ^ P.xin ^ P.vfix) & ~P.vfree & P.outer) != 0);
+}
+
 // Hand buffer j % NBUF over to tile j (issued by the group that held it): load tile j into it, or
 // (F_INIT: nothing to load) just arrive.  Called by all NT threads of the issuing group.
 template <typename V>
@@ -725,8 +735,8 @@ __device__ __forceinline__ void issue_tile(V *smbase, uint64_t *mbar, const V *p
 {
     if (cta_tile(j, P) == ~0ull) return;
     const int b = (int)(j % NBUF);
-    if (init) {
-        mbar_arrive(&mbar[j % NMB]);
+    if (init || tile_dead(tbase, P)) {   // nothing to load: just arrive (one arrival per bulk phase)
+        if (!(P.flags & F_BULK) || tid == 0) mbar_arrive(&mbar[j % NMB]);
     } else if (P.flags & F_BULK) {
         // the tile is one contiguous 64 KiB (c128) block: ONE bulk copy (TMA engine, UBLKCP)
         // issued by one thread, completion as transaction bytes on the buffer's mbarrier
@@ -849,12 +859,13 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         const uint64_t bout = lookup(tabo, T);
         const uint64_t blog = need_l ? lookup(tabl, T) : 0;
         mbar_wait(&mbar[j % NMB], (uint32_t)((j / NMB) & 1));
-        if (init) {
+        const bool dead = tile_dead(base, P);
+        if (init || dead) {
             // a reset: every amplitude is 0 but one, whose place in the phase-0 layout (after any
             // leading transposes, folded away on the host) the planner computed
 #pragma unroll
             for (int r = 0; r < NR; ++r) { a[r].x = R(0); a[r].y = R(0); }
-            if (tid == P.init_t) {   // (F_INIT comes with F_LIVE: T is the one live tile)
+            if (init && tid == P.init_t) {   // (F_INIT comes with F_LIVE: T is the one live tile)
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
                     if ((uint32_t)r == P.init_r) { a[r].x = (R)P.init_re; a[r].y = (R)P.init_im; }
@@ -880,7 +891,20 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                 for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + (t0 ^ P.ph[0].so[r]));
             }
         }
-        if (P.last_xpose == 0xFFFFu) {   // no transpose in this group: release the buffer right away
+        if ((P.flags & F_VMASK) && !init && !dead) {
+            // elements the buffer does not hold (outside the valid set) are zero
+            uint32_t tl0 = 0;
+#pragma unroll
+            for (int q = 0; q < NTB; ++q) tl0 |= ((tid >> q) & 1u) << P.ph[0].tl[q];
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                const uint32_t e = P.gtab != 0xFFFFu
+                                       ? swz((uint32_t)gsm[r * NT + tid] / (uint32_t)sizeof(V)) ^ P.mloc
+                                       : tl0 ^ ((uint32_t)P.so0[r] / (uint32_t)sizeof(V));
+                if ((e & P.vl_mask) != P.vl_val) { a[r].x = R(0); a[r].y = R(0); }
+            }
+        }
+        if (P.last_xpose == 0xFFFFu || dead) {   // no transpose in this group: release the buffer right away
             if (P.flags & F_BULK) fence_proxy_async();
             named_bar(bar);
             issue_tile(smbase, mbar, src, j + NBUF, nbase, P, gt, tid, init);
@@ -895,8 +919,9 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
         // -> branch chain was the top stall in ncu's source view; a shared-memory copy fetched by
         // a volatile load at the top of the iteration measured ~6 % slower)
         const uint64_t *recw = reinterpret_cast<const uint64_t *>(P.g);
-        uint64_t wnext = P.ngate ? recw[0] : 0;
-        for (uint32_t gi = 0; gi < P.ngate; ++gi) {
+        const uint32_t ngate = dead ? 0u : P.ngate;   // a zero tile stays zero
+        uint64_t wnext = ngate ? recw[0] : 0;
+        for (uint32_t gi = 0; gi < ngate; ++gi) {
             const uint64_t w = wnext;
             wnext = recw[gi + 1 < P.ngate ? gi + 1 : gi];
             GRec g;
@@ -1086,6 +1111,15 @@ void GateTimer::flush()
         }
     }
     used_ = 0;
+}
+
+// deposit the low bits of x into the set bits of m (host pdep)
+static uint64_t pdep_mask(uint64_t x, uint64_t m)
+{
+    uint64_t o = 0;
+    for (; m && x; m &= m - 1, x >>= 1)
+        if (x & 1) o |= m & (~m + 1);
+    return o;
 }
 
 static void count(Ctx &ctx, double bytes, bool fused)
@@ -2172,8 +2206,6 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         while (KP < NLG && __builtin_popcountll(supS[KP] & ~tiles[KP] & all) + 3 <= (int)(n_ - TB)) ++KP;
         if (KP == 0 && pending_init && NLG) KP = 1;   // the reset group itself is always one tile
     }
-    // the part of the buffer a reset must zero: what the previous call may have left nonzero
-    const uint64_t zfree = dfree_ & all, zfix = dfix_ & all & ~zfree;
     std::vector<std::array<uint8_t, 64>> lay(NLG + 1);
 #ifdef TUSQ_DEBUG_KNOBS   // debug builds only: TUSQ_DBG_IDENTITY=1 keeps every layout the identity
     static const bool dbg_identity = getenv("TUSQ_DBG_IDENTITY") != nullptr;
@@ -2426,9 +2458,31 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         const bool last = gi + 1 == groups.size();
         bool want = last && d_sums && B.tile == ((1ull << TB) - 1);
         if (want) P.flags |= F_SUMS;
-        const double zbytes = __builtin_popcountll(zfree) + 2 <= (int)n_
-                                  ? (double)(1ull << __builtin_popcountll(zfree)) * (prec_ == 128 ? 16 : 8) : s;
-        const double bytes = pending_init ? zbytes : (P.flags & F_LIVE) ? 2.0 * (double)P.nlive * tbytes : 2 * s;
+        // F_VMASK: the first sweep reading a buffer that is valid on V only (identity read layout)
+        const bool vmask = !pending_init && (vfree_ & all) != all;
+        if (vmask) {
+            for (int b = 0; b < TB; ++b)
+                if (P.pin[b] != P.qs[b])
+                    throw std::runtime_error("fused planner: valid-set sweep outside the identity layout");
+            P.flags |= F_VMASK;
+            P.vfree = vfree_ & all;
+            P.vfix = vfix_ & all & ~P.vfree;
+            P.vl_mask = P.vl_val = 0;
+            for (int b = 0; b < TB; ++b)
+                if (!((P.vfree >> P.pin[b]) & 1)) {
+                    P.vl_mask |= 1u << b;
+                    P.vl_val |= (uint32_t)((P.vfix >> P.pin[b]) & 1) << b;
+                }
+        }
+        // bytes: a reset sweep writes one tile; live sweeps move their tiles; a full sweep on a
+        // partly valid buffer reads only the tiles V touches
+        double bytes = 2 * s;
+        if (pending_init) bytes = tbytes;
+        else if (P.flags & F_LIVE) bytes = 2.0 * (double)P.nlive * tbytes;
+        else if (vmask) {
+            const int vout = __builtin_popcountll(P.vfree & P.outer);
+            bytes = s + (double)(1ull << vout) * tbytes;
+        }
         if (!ctx.dry) {
             int bps = blocks_per_sm(prec_);
             const uint64_t nt = (P.flags & F_LIVE) ? P.nlive : P.ntiles;
@@ -2464,14 +2518,9 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                     P.ph[k].so_out[r] = (uint16_t)(P.ph[k].so_out[r] * esz);
                 }
             if (ctx.timer) ctx.timer->begin(ctx.st);
-            if (pending_init) {
-                // A reset sweep: the group's gates act inside tiles, so every tile but the one holding
-                // the basis state stays zero.  K7 writes the zeros at streaming-store speed, then ONE
-                // CTA computes that tile (F_LIVE, nlive = 1).  (Every tile computing its zeros in its
-                // own write layout measured 2.7-4.0 ms at n = 30; K7 alone is ~2.5 ms.)
-                if (__builtin_popcountll(zfree) + 2 <= (int)n_) launch_zero_affine(dst, n_, prec_, zfree, zfix, ctx.st);
-                else launch_init_basis(dst, n_, prec_, 0, 0.0, 0.0, ctx.st);
-            }
+            // A reset sweep is ONE CTA computing the tile that holds the basis state (F_LIVE,
+            // nlive = 1); the rest of the buffer is not written -- the valid set V shrinks to that
+            // tile (the zeros outside V are only written by finish(), once per call).
             // live-tile sweeps write the sums of their live tiles only: the others are zero
             if ((P.flags & F_LIVE) && want &&
                 cudaMemsetAsync(d_sums, 0, (size_t)P.ntiles * sizeof(double), ctx.st) != cudaSuccess)
@@ -2506,8 +2555,18 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
 #endif
         }
         count(ctx, bytes, true);
-        if (pending_init) ctx.stats->launches++;   // the K7 zero fill before the one-CTA sweep
         pending_init = false;
+        // the valid set after this sweep: a live sweep (in place, identity layout) wrote its live
+        // tiles whole; any other sweep wrote every tile
+        if (P.flags & F_LIVE) {
+            uint64_t tpos = 0;
+            for (int b = 0; b < TB; ++b) tpos |= bit(P.pin[b]);
+            vfree_ = tpos | pdep_mask(P.lfree, P.outer);
+            vfix_ = (pdep_mask(P.lfix, P.outer) ^ P.xin) & ~vfree_ & all;
+        } else {
+            vfree_ = ~0ull;
+            vfix_ = 0;
+        }
         xmask_ = P.xm_store ^ G.xa;
         if (want && sums_written) *sums_written = true;
     }
@@ -2526,12 +2585,39 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
 void FusedPlanner::materialize(Ctx &ctx)
 {
     if (!xmask_) return;
-    dfix_ ^= xmask_ & ~dfree_;   // the XOR moves the known support with the state
+    dfix_ ^= xmask_ & ~dfree_;   // the XOR moves the known support and the valid set with the state
+    vfix_ ^= xmask_ & ~vfree_;
     double b = 0;
     if (!ctx.dry) b = launch_pauli_string(ctx.psi, n_, prec_, xmask_, 0, ctx.st);
     else b = 2.0 * (double)(1ull << n_) * (prec_ == 128 ? 16 : 8);
     count(ctx, b, false);
     xmask_ = 0;
+}
+
+void FusedPlanner::close_blocks(Ctx &ctx, uint32_t block_bits)
+{
+    const uint64_t all = n_ >= 64 ? ~0ull : (1ull << n_) - 1, low = (1ull << block_bits) - 1;
+    if ((vfree_ & all) == all || (vfree_ & low) == low) return;
+    // zeros in the blocks V touches, at the elements outside V; V becomes those whole blocks
+    const uint64_t sf = (vfree_ & all) | low;
+    double b = 0;
+    if (!ctx.dry) b = launch_zero_outside(ctx.psi, n_, prec_, sf, vfix_ & all & ~sf, vfree_ & all, vfix_ & all & ~vfree_, ctx.st);
+    else b = (double)(1ull << __builtin_popcountll(sf)) * (prec_ == 128 ? 16 : 8);
+    count(ctx, b, false);
+    vfree_ = sf;
+    vfix_ &= ~sf;
+}
+
+void FusedPlanner::finish(Ctx &ctx)
+{
+    const uint64_t all = n_ >= 64 ? ~0ull : (1ull << n_) - 1;
+    if ((vfree_ & all) == all) return;
+    double b = 0;
+    if (!ctx.dry) b = launch_zero_outside(ctx.psi, n_, prec_, all, 0, vfree_ & all, vfix_ & all & ~vfree_, ctx.st);
+    else b = (double)(1ull << n_) * (prec_ == 128 ? 16 : 8);
+    count(ctx, b, false);
+    vfree_ = ~0ull;
+    vfix_ = 0;
 }
 
 }  // namespace tq

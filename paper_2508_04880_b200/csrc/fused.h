@@ -77,7 +77,16 @@ public:
     void materialize(Ctx &ctx);
     void reset_mask() { xmask_ = 0; }
     // the caller wrote the basis state |index> (K7) into the state: the known support is one element
-    void note_basis(uint64_t index) { xmask_ = 0; dfree_ = 0; dfix_ = index; }
+    // and the whole buffer is valid
+    void note_basis(uint64_t index) { xmask_ = 0; dfree_ = 0; dfix_ = index; vfree_ = ~0ull; vfix_ = 0; }
+    // The buffer may hold the state only on a valid set V = {x : (x & ~vfree) == vfix} (physical,
+    // identity layout; outside it the state is zero and the buffer stale).  Readers outside K5:
+    // close_blocks() makes V a union of whole 2^12-element blocks (zeros written inside the blocks
+    // V touches) before the sampler's block sums, which skip the blocks outside V; finish() writes
+    // the zeros outside V so the caller's buffer holds the whole state.
+    void valid_set(uint64_t *vfree, uint64_t *vfix) const { *vfree = vfree_; *vfix = vfix_; }
+    void close_blocks(Ctx &ctx, uint32_t block_bits);
+    void finish(Ctx &ctx);
 
 private:
     uint32_t n_;
@@ -88,6 +97,7 @@ private:
     // known support of the state in ctx.psi (physical positions, identity layout): every nonzero
     // amplitude has (index & ~dfree_) == dfix_; dfree_ = ~0 when unknown
     uint64_t dfree_ = ~0ull, dfix_ = 0;
+    uint64_t vfree_ = ~0ull, vfix_ = 0;   // the valid set V (see valid_set)
     void *alt_ = nullptr;
     uint64_t alt_lazy_ = 0;
     bool alt_owned_ = false;

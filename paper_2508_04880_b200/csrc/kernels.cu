@@ -328,33 +328,43 @@ double launch_pauli_string(void *psi, uint32_t n, int prec, uint64_t xm, uint64_
     return prec == 64 ? pauli_impl<float>(psi, n, xm, zm, st) : pauli_impl<double>(psi, n, xm, zm, st);
 }
 
-// zeros at every index x with (x & ~free) == fix: the part of a state that may be nonzero when a
-// support analysis bounds it (K5 live tiles), written before a reset instead of the whole state
+// zeros at the elements x of the affine set {x : (x & ~scan_free) == scan_fix} that lie OUTSIDE the
+// valid set {x : (x & ~vfree) == vfix}: K5's live-tile sweeps leave stale data outside the valid
+// set; this writes the zeros there (a whole-state pass at the end of a call, or the blocks the
+// valid set touches before the sampler reads them)
 template <typename V>
-__global__ void __launch_bounds__(TPB) k_zero_affine(V *__restrict__ psi, uint64_t cnt, uint64_t free, uint64_t fix)
+__global__ void __launch_bounds__(TPB) k_zero_outside(V *__restrict__ psi, uint64_t cnt, uint64_t sfree, uint64_t sfix,
+                                                      uint64_t vfree, uint64_t vfix, bool dense)
 {
     for (uint64_t i = (uint64_t)blockIdx.x * TPB + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * TPB) {
-        uint64_t o = fix, x = i;
-        for (uint64_t m = free; m && x; m &= m - 1, x >>= 1)
-            if (x & 1) o |= m & (~m + 1);
-        V z;
-        z.x = 0;
-        z.y = 0;
-        psi[o] = z;
+        uint64_t x = i;
+        if (!dense) {
+            x = sfix;
+            uint64_t y = i;
+            for (uint64_t m = sfree; m && y; m &= m - 1, y >>= 1)
+                if (y & 1) x |= m & (~m + 1);
+        }
+        if ((x ^ vfix) & ~vfree) {
+            V z;
+            z.x = 0;
+            z.y = 0;
+            __stcs(psi + x, z);
+        }
     }
 }
 
-double launch_zero_affine(void *psi, uint32_t n, int prec, uint64_t free, uint64_t fix, cudaStream_t st)
+double launch_zero_outside(void *psi, uint32_t n, int prec, uint64_t sfree, uint64_t sfix, uint64_t vfree, uint64_t vfix,
+                           cudaStream_t st)
 {
     const uint64_t all = n >= 64 ? ~0ull : (1ull << n) - 1;
-    free &= all;
-    fix &= all & ~free;
-    const uint64_t cnt = 1ull << __builtin_popcountll(free);
+    sfree &= all;
+    const uint64_t cnt = 1ull << __builtin_popcountll(sfree);
+    const bool dense = sfree == all;
     if (prec == 64) {
-        k_zero_affine<float2><<<grid_for(cnt, TPB, 1), TPB, 0, st>>>((float2 *)psi, cnt, free, fix);
+        k_zero_outside<float2><<<grid_for(cnt, TPB, 1), TPB, 0, st>>>((float2 *)psi, cnt, sfree, sfix, vfree, vfix, dense);
         return cnt * 8.0;
     }
-    k_zero_affine<double2><<<grid_for(cnt, TPB, 1), TPB, 0, st>>>((double2 *)psi, cnt, free, fix);
+    k_zero_outside<double2><<<grid_for(cnt, TPB, 1), TPB, 0, st>>>((double2 *)psi, cnt, sfree, sfix, vfree, vfix, dense);
     return cnt * 16.0;
 }
 
@@ -375,13 +385,19 @@ double launch_init_basis(void *psi, uint32_t n, int prec, uint64_t index, double
 // blocks and a warp-shuffle scan inside the chosen block.  Sums in fp64 for both precisions.
 template <typename R, int PER>
 __global__ void __launch_bounds__(TPB) k_block_sums(const typename CV<R>::T *__restrict__ psi, uint32_t block_bits,
-                                                    double *__restrict__ out)
+                                                    double *__restrict__ out, uint64_t vfree, uint64_t vfix)
 {
     // PER > 0: the block is PER * TPB amplitudes and every load is issued before the first use
     // (PER independent 16-byte loads in flight per thread); PER = 0: generic strided loop
     using V = typename CV<R>::T;
     const uint64_t bs = 1ull << block_bits;
     const uint64_t base = (uint64_t)blockIdx.x * bs;
+    // a block outside the valid set holds no amplitude (K5 live tiles: the buffer is stale there;
+    // the valid set covers whole blocks when the sampler runs, FusedPlanner::close_blocks)
+    if ((base ^ vfix) & ~vfree & ~(bs - 1)) {
+        if (threadIdx.x == 0) out[blockIdx.x] = 0.0;
+        return;
+    }
     double acc = 0.0;
     if constexpr (PER > 0) {
         V a[PER];
@@ -411,18 +427,19 @@ __global__ void __launch_bounds__(TPB) k_block_sums(const typename CV<R>::T *__r
 }
 
 double launch_block_sums(const void *psi, uint32_t n, int prec, uint32_t block_bits, double *d_blocks,
-                         cudaStream_t st)
+                         cudaStream_t st, uint64_t vfree, uint64_t vfix)
 {
     uint64_t nb = 1ull << (n - block_bits);
     const bool fast = block_bits == 12;
     if (prec == 64) {
-        if (fast) k_block_sums<float, 16><<<(unsigned)nb, TPB, 0, st>>>((const float2 *)psi, block_bits, d_blocks);
-        else k_block_sums<float, 0><<<(unsigned)nb, TPB, 0, st>>>((const float2 *)psi, block_bits, d_blocks);
+        if (fast) k_block_sums<float, 16><<<(unsigned)nb, TPB, 0, st>>>((const float2 *)psi, block_bits, d_blocks, vfree, vfix);
+        else k_block_sums<float, 0><<<(unsigned)nb, TPB, 0, st>>>((const float2 *)psi, block_bits, d_blocks, vfree, vfix);
     } else {
-        if (fast) k_block_sums<double, 16><<<(unsigned)nb, TPB, 0, st>>>((const double2 *)psi, block_bits, d_blocks);
-        else k_block_sums<double, 0><<<(unsigned)nb, TPB, 0, st>>>((const double2 *)psi, block_bits, d_blocks);
+        if (fast) k_block_sums<double, 16><<<(unsigned)nb, TPB, 0, st>>>((const double2 *)psi, block_bits, d_blocks, vfree, vfix);
+        else k_block_sums<double, 0><<<(unsigned)nb, TPB, 0, st>>>((const double2 *)psi, block_bits, d_blocks, vfree, vfix);
     }
-    return (double)(1ull << n) * (prec == 64 ? 8.0 : 16.0);
+    const uint64_t all = n >= 64 ? ~0ull : (1ull << n) - 1;
+    return (double)(1ull << __builtin_popcountll((vfree & all) | ((1ull << block_bits) - 1))) * (prec == 64 ? 8.0 : 16.0);
 }
 
 // Two-level CDF over blocks: superblocks of SB logical blocks.  k_super sums each superblock

@@ -13,13 +13,15 @@ double launch_gate(void *psi, uint32_t n, int prec, const Op &op, cudaStream_t s
 double launch_pauli_string(void *psi, uint32_t n, int prec, uint64_t xmask, uint64_t zmask, cudaStream_t st);
 // K7: psi <- amp |index>
 double launch_init_basis(void *psi, uint32_t n, int prec, uint64_t index, double re, double im, cudaStream_t st);
-// zeros on the affine set {x : (x & ~free) == fix} (the part a support analysis says may be nonzero)
-double launch_zero_affine(void *psi, uint32_t n, int prec, uint64_t free, uint64_t fix, cudaStream_t st);
+// zeros at the elements of {x : (x & ~sfree) == sfix} outside the valid set {x : (x & ~vfree) == vfix}
+double launch_zero_outside(void *psi, uint32_t n, int prec, uint64_t sfree, uint64_t sfix, uint64_t vfree, uint64_t vfix,
+                           cudaStream_t st);
 
 // ----- K6: sampler ---------------------------------------------------------------------
-// block sums of |amp|^2 over contiguous blocks of 2^block_bits amplitudes
+// block sums of |amp|^2 over contiguous blocks of 2^block_bits amplitudes; blocks outside the valid
+// set {x : (x & ~vfree) == vfix} (whole blocks) sum to 0 unread
 double launch_block_sums(const void *psi, uint32_t n, int prec, uint32_t block_bits, double *d_blocks,
-                         cudaStream_t st);
+                         cudaStream_t st, uint64_t vfree = ~0ull, uint64_t vfix = 0);
 // superblock (1024 logical blocks) sums of nb block sums given in PHYSICAL order (physical block =
 // logical ^ mh), then their exclusive prefix: d_prefix[0..nsb] (nsb = ceil(nb/1024)); needs
 // 2*nsb + 2 doubles of d_prefix
