@@ -610,6 +610,19 @@ __device__ __forceinline__ void cp_async(void *smem, const void *gmem)
     if constexpr (BYTES == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
     else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
+// the same copy, or (skip) zeros written without reading global memory (the ignore-src operand)
+template <int BYTES>
+__device__ __forceinline__ void cp_async_or_zero(void *smem, const void *gmem, bool skip)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned k = skip;
+    if constexpr (BYTES == 16)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+                     "cp.async.cg.shared.global [%0], [%1], 16, p;\n\t}" ::"r"(s), "l"(gmem), "r"(k));
+    else
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+                     "cp.async.ca.shared.global [%0], [%1], 8, p;\n\t}" ::"r"(s), "l"(gmem), "r"(k));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -636,8 +649,18 @@ __device__ __forceinline__ void prefetch_tile(V *sm, const V *psi, uint64_t tbas
     const char *src = reinterpret_cast<const char *>(psi + ((tbase ^ P.xin) + gt));
     char *dst = reinterpret_cast<char *>(sm);
     const uint32_t st = swz(tid ^ P.mloc) * (uint32_t)sizeof(V);
+    if (P.flags & F_VMASK) {
+        // the buffer holds the state only on the valid set: elements outside it are zero, written
+        // into shared memory without a global read
 #pragma unroll
-    for (int j = 0; j < NR; ++j) cp_async<sizeof(V)>(dst + (st ^ P.sj[j]), src + P.gj[j]);
+        for (int j = 0; j < NR; ++j) {
+            const uint32_t e = tid + (uint32_t)NT * (uint32_t)j;   // physical tile-local index
+            cp_async_or_zero<sizeof(V)>(dst + (st ^ P.sj[j]), src + P.gj[j], (e & P.vl_mask) != P.vl_val);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) cp_async<sizeof(V)>(dst + (st ^ P.sj[j]), src + P.gj[j]);
+    }
     cp_async_commit();
 }
 
@@ -889,19 +912,6 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                 t0 = swz(t0) * (uint32_t)sizeof(V);
 #pragma unroll
                 for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + (t0 ^ P.ph[0].so[r]));
-            }
-        }
-        if ((P.flags & F_VMASK) && !init && !dead) {
-            // elements the buffer does not hold (outside the valid set) are zero
-            uint32_t tl0 = 0;
-#pragma unroll
-            for (int q = 0; q < NTB; ++q) tl0 |= ((tid >> q) & 1u) << P.ph[0].tl[q];
-#pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                const uint32_t e = P.gtab != 0xFFFFu
-                                       ? swz((uint32_t)gsm[r * NT + tid] / (uint32_t)sizeof(V)) ^ P.mloc
-                                       : tl0 ^ ((uint32_t)P.so0[r] / (uint32_t)sizeof(V));
-                if ((e & P.vl_mask) != P.vl_val) { a[r].x = R(0); a[r].y = R(0); }
             }
         }
         if (P.last_xpose == 0xFFFFu || dead) {   // no transpose in this group: release the buffer right away
@@ -2280,6 +2290,9 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         // arbitrary slots and keeps the swizzled staging (ncu: 7x bank conflicts from linear)
         if (((1u << P.ph[0].tl[0]) | (1u << P.ph[0].tl[1]) | (1u << P.ph[0].tl[2])) != 7u) bulk = false;
         if (P.ngate && P.g[0].code == C_XPOSE) bulk = false;
+        // a buffer valid on a subset only is read element-wise (invalid elements zero-filled)
+        if (!pending_init && (vfree_ & ((n_ >= 64 ? ~0ull : (1ull << n_) - 1))) != (n_ >= 64 ? ~0ull : (1ull << n_) - 1))
+            bulk = false;
         {
             const Phase &f = P.ph[0], &l = P.ph[P.nphase - 1];
             P.regm_load = 0;
@@ -2479,10 +2492,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         double bytes = 2 * s;
         if (pending_init) bytes = tbytes;
         else if (P.flags & F_LIVE) bytes = 2.0 * (double)P.nlive * tbytes;
-        else if (vmask) {
-            const int vout = __builtin_popcountll(P.vfree & P.outer);
-            bytes = s + (double)(1ull << vout) * tbytes;
-        }
+        else if (vmask) bytes = s + (double)(1ull << __builtin_popcountll(P.vfree)) * (prec_ == 128 ? 16 : 8);
         if (!ctx.dry) {
             int bps = blocks_per_sm(prec_);
             const uint64_t nt = (P.flags & F_LIVE) ? P.nlive : P.ntiles;
@@ -2547,9 +2557,9 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 }
                 int contig = 1;
                 for (int b = 0; b < TB; ++b) contig &= P.pin[b] == b;
-                fprintf(stderr, "[k5] idx %d ops %zu recs %u ph %u init %d contig %d oop %d gtab %d tile %#llx H %d DK %d CX %d D %d XP %d XY %d TP %d O %d CU %d CCX %d\n",
+                fprintf(stderr, "[k5] idx %d ops %zu recs %u ph %u init %d contig %d oop %d gtab %d nlive %llu vmask %d tile %#llx H %d DK %d CX %d D %d XP %d XY %d TP %d O %d CU %d CCX %d\n",
                         ctx.timer ? (int)ctx.timer->pending() - 1 : -1, G.ops.size(), P.ngate, P.nphase, pending_init ? 1 : 0, contig, src != dst ? 1 : 0,
-                        P.gtab != 0xFFFFu, (unsigned long long)B.tile, cnt[0], cnt[1], cnt[2], cnt[3], cnt[4], cnt[5],
+                        P.gtab != 0xFFFFu, (unsigned long long)((P.flags & F_LIVE) ? P.nlive : P.ntiles), (P.flags & F_VMASK) ? 1 : 0, (unsigned long long)B.tile, cnt[0], cnt[1], cnt[2], cnt[3], cnt[4], cnt[5],
                         cnt[6], cnt[7], cnt[8], cnt[9]);
             }
 #endif
