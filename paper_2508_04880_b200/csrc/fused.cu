@@ -136,7 +136,8 @@ struct GRec {
     uint16_t _pad;
 };
 
-enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8, F_BULK = 16, F_LIVE = 32, F_VMASK = 64 };
+enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8, F_BULK = 16, F_LIVE = 32, F_VMASK = 64, F_TSTORE = 128,
+                  F_DBG_NOSTORE = 1u << 31 };   // (debug-knob builds only: skip the stores, for timing)
 constexpr int NCH = 4;             // 8-bit chunks of the tile index (n <= TB + 8 * NCH = 44 fused)
 
 // Qubit layout: the state may be stored with its qubits permuted (logical qubit q at physical bit
@@ -156,6 +157,14 @@ struct Params {
                                   //   {x : (x & ~vfree) == vfix}; elsewhere it is zero but not written:
                                   //   tiles outside are not loaded (zeros), elements outside read as 0
     uint32_t vl_mask, vl_val;     //   the same condition on the tile-local bits
+    // F_TSTORE: the tile is written through shared memory by bulk copies (TMA engine): registers go
+    // to the tile buffer in WRITE order (tile bits sorted by write position), whose runs of 2^ts_l0
+    // elements are contiguous in both places; run i lands at the tile base + pdep(i, ts_hi) where
+    // ts_hi holds the write positions of write-order bits ts_l0..11
+    uint8_t ts_l0;
+    uint8_t ts_hipos[TB];         //   write position of write-order bit ts_l0 + k
+    uint8_t wpos[TB];             //   write-order bit of tile-local bit b
+    uint16_t wreg[NR];            //   write-order offset (bytes at launch) of register r in the last phase
     double init_re, init_im;
     double scale_re, scale_im;
     uint64_t ntiles;
@@ -821,6 +830,16 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
     // tile index -> write-layout / logical base: one table per 8-bit chunk of the tile index
     uint64_t(*tabo)[256] = reinterpret_cast<uint64_t(*)[256]>(gsm + NR * NT);
     uint64_t(*tabl)[256] = tabo + NCH;
+    uint64_t *rofs = reinterpret_cast<uint64_t *>(tabl + NCH);   // F_TSTORE: run offsets (bytes)
+    if (P.flags & F_TSTORE) {
+        const uint32_t nrun = 1u << (TB - P.ts_l0);
+        for (uint32_t i = threadIdx.x; i < nrun; i += NT * NG) {
+            uint64_t o = 0;
+            for (uint32_t k = 0; k < (uint32_t)(TB - P.ts_l0); ++k)
+                if ((i >> k) & 1u) o |= 1ull << P.ts_hipos[k];
+            rofs[i] = o * sizeof(V);
+        }
+    }
     const bool need_l = P.flags & F_LBASE;
     for (uint32_t i = threadIdx.x; i < NCH * 256; i += NT * NG) {
         const uint32_t c = i >> 8, v = i & 255u;
@@ -914,7 +933,8 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                 for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + (t0 ^ P.ph[0].so[r]));
             }
         }
-        if (P.last_xpose == 0xFFFFu || dead) {   // no transpose in this group: release the buffer right away
+        const bool tstore = P.flags & F_TSTORE;   // (the buffer then stays ours until the stores read it)
+        if (!tstore && (P.last_xpose == 0xFFFFu || dead)) {   // no transpose: release the buffer right away
             if (P.flags & F_BULK) fence_proxy_async();
             named_bar(bar);
             issue_tile(smbase, mbar, src, j + NBUF, nbase, P, gt, tid, init);
@@ -977,7 +997,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
 #pragma unroll
                     for (int q = 0; q < NTB; ++q) lbase |= (uint64_t)((tid >> q) & 1u) << P.qs[cur.tl[q]];
                 }
-                if (gi == P.last_xpose) {   // the buffer is free until tile j + NBUF: hand it over
+                if (gi == P.last_xpose && !tstore) {   // the buffer is free until tile j + NBUF: hand it over
                     if (P.flags & F_BULK) fence_proxy_async();
                     named_bar(bar);
                     issue_tile(smbase, mbar, src, j + NBUF, nbase, P, gt, tid, init);
@@ -996,8 +1016,37 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                 for (int r = 0; r < NR; ++r) cmul_ip(a[r], sr, si);
             }
         }
+        if (tstore) {
+            // registers -> the tile buffer in write order, then bulk copies of its contiguous runs
+            named_bar(bar);   // everyone is done reading the buffer
+            uint32_t wt = 0;
+#pragma unroll
+            for (int q = 0; q < NTB; ++q) wt |= ((tid >> q) & 1u) << P.wpos[P.ph[P.nphase - 1].tl[q]];
+            wt *= (uint32_t)sizeof(V);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) *reinterpret_cast<V *>(smb + (wt ^ P.wreg[r])) = a[r];
+            fence_proxy_async();
+            named_bar(bar);
+            const uint32_t nrun = 1u << (TB - P.ts_l0), rbytes = (1u << P.ts_l0) * (uint32_t)sizeof(V);
+            char *tb = reinterpret_cast<char *>(dst + (bout ^ P.xout));
+            const unsigned sbase = (unsigned)__cvta_generic_to_shared(smb);
+            for (uint32_t i = tid; i < nrun; i += NT)
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(tb + rofs[i]),
+                             "r"(sbase + i * rbytes), "r"(rbytes)
+                             : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            named_bar(bar);   // the buffer has been read: hand it to tile j + NBUF
+            issue_tile(smbase, mbar, src, j + NBUF, nbase, P, gt, tid, init);
+        }
         // xout has no tile bits: register offsets are additive
         V *q0 = dst + ((bout | gthr_st) ^ P.xout);
+#ifdef TUSQ_DEBUG_KNOBS
+        if (P.flags & F_DBG_NOSTORE) {
+            if (a[0].x == R(12345)) q0[0] = a[1];   // keep the registers live
+            continue;
+        }
+#endif
 #ifdef TUSQ_DEBUG_CHECKS
         for (int r = 0; r < NR; ++r)
             if (((bout | gthr_st) ^ P.xout) + P.gs[r] / sizeof(V) >= (P.ntiles << TB)) {
@@ -1005,7 +1054,9 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                 __trap();
             }
 #endif
-        if (P.st_pair) {
+        if (tstore) {
+            // (written above)
+        } else if (P.st_pair) {
             switch (P.st_pair) {
 #define TQ_SP(v) case v: if constexpr (v < NR) store_pairs<v>(q0, a, P); break;
                 TQ_SP(1) TQ_SP(2) TQ_SP(3) TQ_SP(4) TQ_SP(5) TQ_SP(6) TQ_SP(7) TQ_SP(8) TQ_SP(9) TQ_SP(10)
@@ -1039,6 +1090,8 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
             named_bar(bar);
         }
     }
+    // bulk stores still in flight must land before the CTA retires
+    if (P.flags & F_TSTORE) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace fk
@@ -2069,7 +2122,8 @@ static void build_params(const Group &G, uint32_t n, Built &B, uint64_t tile, co
 // dynamic shared memory of k_fused: NBUF tile buffers, the gather table, the tile-index tables
 static size_t smem_bytes(int prec)
 {
-    return (size_t)NBUF * (1 << TB) * (prec == 128 ? 16 : 8) + NR * NT * 2 + 2 * NCH * 256 * sizeof(uint64_t);
+    return (size_t)NBUF * (1 << TB) * (prec == 128 ? 16 : 8) + NR * NT * 2 + 2 * NCH * 256 * sizeof(uint64_t) +
+           (1 << (TB - 3)) * sizeof(uint64_t);   // F_TSTORE run offsets (runs >= 8 elements)
 }
 
 static int blocks_per_sm(int prec)
@@ -2314,6 +2368,24 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 P.gl[r] = goff(f, (uint32_t)B.pin0[r] ^ P.rx, P.qs);
                 P.gs[r] = goff(l, B.pout_last[r], P.pout);
             }
+            // bulk-copy stores (F_TSTORE): write order = tile bits by write position; the low ts_l0
+            // write-order bits must be write positions 0..ts_l0-1 (contiguous, aligned runs)
+            {
+                uint8_t ord[TB];
+                for (int b = 0; b < TB; ++b) ord[b] = (uint8_t)b;
+                std::sort(ord, ord + TB, [&](uint8_t x, uint8_t y) { return P.pout[x] < P.pout[y]; });
+                for (int k = 0; k < TB; ++k) P.wpos[ord[k]] = (uint8_t)k;
+                int l0 = 0;
+                while (l0 < TB && P.pout[ord[l0]] == l0) ++l0;
+                P.ts_l0 = (uint8_t)l0;
+                for (int k = 0; k + l0 < TB; ++k) P.ts_hipos[k] = P.pout[ord[l0 + k]];
+                for (int r = 0; r < NR; ++r) {
+                    uint32_t w = 0;
+                    for (int k = 0; k < RB; ++k)
+                        if ((B.pout_last[r] >> k) & 1) w |= 1u << P.wpos[l.rl[k]];
+                    P.wreg[r] = (uint16_t)w;
+                }
+            }
             P.rx = 0;
             // paired stores when qubit 0 is a register bit of the last layout
             P.st_pair = 0;
@@ -2439,6 +2511,16 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             if ((c >= C_TX && c <= C_TPH) || (c >= C_TDK && c < C_DKC)) P.flags |= F_LBASE;
         }
         if (bulk) P.flags |= F_BULK;
+        {
+            int ts_min = 6;   // stores by bulk copies when runs are >= 2^ts_min elements (measured:
+                              // 64 KiB runs 6.40 -> 5.81 ms, 128-byte runs 7.74 -> 11.5 ms, 1-2 KiB even)
+#ifdef TUSQ_DEBUG_KNOBS       // TUSQ_DBG_TS_L0=k: only runs >= 2^k elements (13: never)
+            static const int dbg_ts = getenv("TUSQ_DBG_TS_L0") ? atoi(getenv("TUSQ_DBG_TS_L0")) : 0;
+            if (dbg_ts) ts_min = dbg_ts;
+#endif
+            // (not on a partly valid buffer: its mostly-zero tiles measured slower with it)
+            if (P.ts_l0 >= ts_min && (vfree_ & all) == all) P.flags |= F_TSTORE;
+        }
         if (pending_init) {
             P.flags |= F_INIT;
             P.init_re = init->re;
@@ -2471,6 +2553,10 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         const bool last = gi + 1 == groups.size();
         bool want = last && d_sums && B.tile == ((1ull << TB) - 1);
         if (want) P.flags |= F_SUMS;
+#ifdef TUSQ_DEBUG_KNOBS   // TUSQ_DBG_NOSTORE=1: the sweeps skip their stores (wrong results; timing only)
+        static const bool dbg_nostore = getenv("TUSQ_DBG_NOSTORE") != nullptr;
+        if (dbg_nostore) P.flags |= F_DBG_NOSTORE;
+#endif
         // F_VMASK: the first sweep reading a buffer that is valid on V only (identity read layout)
         const bool vmask = !pending_init && (vfree_ & all) != all;
         if (vmask) {
@@ -2521,6 +2607,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 P.gj[r] *= esz;
                 P.sj[r] = (uint16_t)(P.sj[r] * esz);
                 P.so0[r] = (uint16_t)(P.so0[r] * esz);
+                P.wreg[r] = (uint16_t)(P.wreg[r] * esz);
             }
             for (uint32_t k = 0; k < P.nphase; ++k)
                 for (int r = 0; r < NR; ++r) {
