@@ -173,6 +173,17 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def dense_line(ptot, peak):
+    """The dense K5 sweeps of the profile pass (every tile of a fully valid state: 2 x 2^n x s bytes)."""
+    if not ptot or not ptot.get("dense_sweep_launches"):
+        return None
+    a = ptot["dense_sweep_bytes"] / ptot["dense_sweep_seconds"] / 1e9
+    return {"launches": int(ptot["dense_sweep_launches"]),
+            "avg_ms": ptot["dense_sweep_seconds"] / ptot["dense_sweep_launches"] * 1e3,
+            "achieved": a, "frac": a / peak,
+            "share_of_K5_time": ptot["dense_sweep_seconds"] / max(ptot["gate_kernel_seconds"], 1e-12)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -304,12 +315,16 @@ def main():
                      "traffic_source": (f"dram__bytes_read.sum + dram__bytes_write.sum of one k_fused launch of this "
                                         f"bench under ncu --set full ({traffic_src})") if traffic_src else None,
                      "kernel": "k_fused (K5)" if not args.no_fuse else "K1-K4",
-                     "per_unit": "one fused sweep = 2 x 2^n x 16 B (2^n x 16 B when it starts from a reset)",
+                     "per_unit": ("one fused sweep = 2 x 2^n x 16 B over every tile it visits: a live-tile sweep "
+                                  "(after a reset) moves 2 x its live tiles x 64 KiB, a reset sweep writes one tile, "
+                                  "the first sweep on a partly valid state writes 2^n x 16 B and reads its valid "
+                                  "elements (DESIGN.md 'Live tiles')"),
                      "launches_profiled": n_launch,
                      "bytes_per_launch": ptot["gate_kernel_bytes"] / max(n_launch, 1) if ptot else None,
                      "avg_launch_ms": ptot["gate_kernel_seconds"] / max(n_launch, 1) * 1e3 if ptot else None,
                      "achieved_in_timed_steps": in_step, "frac_in_timed_steps": in_step / hbm_peak if in_step else None,
-                     "step_share": share_gate, "peak_source": peak_src},
+                     "step_share": share_gate, "peak_source": peak_src,
+                     "dense_sweeps": dense_line(ptot, hbm_peak)},
         "e2e": {"value": wall_max, "unit": "s",
                 "h2d_bytes_per_step": int(tot["h2d_bytes"] / K), "d2h_bytes_per_step": int(tot["d2h_bytes"] / K),
                 "note": "host clock around build_error_tree + every run_tree call (host op list in, host slots out) "

@@ -187,6 +187,10 @@ typedef struct {
     double   d2h_bytes;             /* device -> host bytes of the call (slots, counters) */
     uint64_t sampled_vectors;       /* state vectors sampled (leaves that share a vector under a terminal
                                        relabel count once) */
+    uint64_t dense_sweep_launches;  /* TUSQ_EXEC_PROFILE: K5 launches among gate_kernel_launches that visit
+                                       every tile of a fully valid state (no live-tile / valid-set pruning) */
+    double   dense_sweep_seconds;   /* their summed CUDA-event durations */
+    double   dense_sweep_bytes;     /* their algorithmic HBM bytes (2 x 2^n x amplitude bytes each) */
 } tusq_run_stats;
 
 /* ECM + tree.  ops: n_ops gates (host).  seed keys every Philox stream.

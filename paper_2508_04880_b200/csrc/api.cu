@@ -605,6 +605,9 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
             stats.gate_kernel_seconds = timer.seconds;
             stats.gate_kernel_bytes = timer.bytes;
             stats.sample_kernel_seconds = timer.sample_seconds;
+            stats.dense_sweep_launches = timer.dense_launches;
+            stats.dense_sweep_seconds = timer.dense_seconds;
+            stats.dense_sweep_bytes = timer.dense_bytes;
         }
     } catch (const std::exception &e) {
         cleanup();

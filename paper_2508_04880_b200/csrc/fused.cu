@@ -1165,10 +1165,15 @@ void GateTimer::flush()
         static const bool dbg_trace = getenv("TUSQ_DBG_TRACE") != nullptr;
         if (dbg_trace) fprintf(stderr, "[t] %zu %d %.4f\n", i, (int)cat_[i], ms);
 #endif
-        if (cat_[i] == 0) {
+        if (cat_[i] == 0 || cat_[i] == 2) {   // 2: a dense K5 sweep (also a gate kernel)
             seconds += ms * 1e-3;
             bytes += by_[i];
             ++launches;
+            if (cat_[i] == 2) {
+                dense_seconds += ms * 1e-3;
+                dense_bytes += by_[i];
+                ++dense_launches;
+            }
         } else {
             sample_seconds += ms * 1e-3;
         }
@@ -2628,7 +2633,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             else
                 k_fused<float><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((const float2 *)src, (float2 *)dst, P,
                                                                           d_sums);
-            if (ctx.timer) ctx.timer->end(ctx.st, bytes);
+            if (ctx.timer) ctx.timer->end(ctx.st, bytes, (P.flags & (F_LIVE | F_VMASK | F_INIT)) ? 0 : 2);
 #ifdef TUSQ_DEBUG_KNOBS   // TUSQ_DBG_TRACE=1: one line per K5 launch (group shape), for launch-time fits
             static const bool dbg_trace = getenv("TUSQ_DBG_TRACE") != nullptr;
             if (dbg_trace) {

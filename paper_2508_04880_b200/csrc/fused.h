@@ -21,8 +21,8 @@ public:
     void end(cudaStream_t st, double bytes, int cat = 0);
     void flush();                 // synchronizes the recorded events and accumulates
     size_t pending() const { return used_; }
-    uint64_t launches = 0;
-    double seconds = 0.0, bytes = 0.0, sample_seconds = 0.0;
+    uint64_t launches = 0, dense_launches = 0;
+    double seconds = 0.0, bytes = 0.0, sample_seconds = 0.0, dense_seconds = 0.0, dense_bytes = 0.0;
 
 private:
     bool on_;

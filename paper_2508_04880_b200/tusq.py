@@ -59,7 +59,8 @@ class RunStats(C.Structure):
                 ("fused_launches", C.c_uint64), ("exchanges", C.c_uint64),
                 ("sample_kernel_seconds", C.c_double), ("device_seconds", C.c_double),
                 ("reduce_seconds", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double),
-                ("sampled_vectors", C.c_uint64)]
+                ("sampled_vectors", C.c_uint64), ("dense_sweep_launches", C.c_uint64),
+                ("dense_sweep_seconds", C.c_double), ("dense_sweep_bytes", C.c_double)]
 
     def to_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
