@@ -2241,7 +2241,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     // (dfree_ / dfix_: physical, identity layout; logical = physical ^ xmask_).
     const uint64_t all = n_ >= 64 ? ~0ull : (1ull << n_) - 1;
     std::vector<uint64_t> supS(NLG, ~0ull), supB(NLG, 0);
-    size_t KP = 0;
+    std::vector<char> live(NLG, 0);   // launched group k visits only its live tiles (in place)
     const bool track = pending_init || (dfree_ & all) != all;
     uint64_t sup_end = all, bx_end = 0;
     if (track) {
@@ -2272,8 +2272,9 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         }
         sup_end = sup;
         bx_end = bx;
-        while (KP < NLG && __builtin_popcountll(supS[KP] & ~tiles[KP] & all) + 3 <= (int)(n_ - TB)) ++KP;
-        if (KP == 0 && pending_init && NLG) KP = 1;   // the reset group itself is always one tile
+        // live: the group's live tiles are <= 1/8 of all (the reset group is always one tile)
+        for (size_t g = 0; g < NLG; ++g)
+            live[g] = __builtin_popcountll(supS[g] & ~tiles[g] & all) + 3 <= (int)(n_ - TB) || (g == 0 && pending_init);
     }
     std::vector<std::array<uint8_t, 64>> lay(NLG + 1);
 #ifdef TUSQ_DEBUG_KNOBS   // debug builds only: TUSQ_DBG_IDENTITY=1 keeps every layout the identity
@@ -2288,7 +2289,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     const bool remap = alt_ != nullptr && !dbg_identity && NLG >= 2;
     for (size_t k = 0; k <= NLG; ++k) {
         auto &L = lay[k];
-        if (k <= KP || k == NLG || !remap) {   // (live-tile sweeps run in place: identity)
+        if (k == 0 || k == NLG || !remap || live[k - 1] || live[k]) {   // (live sweeps: in place, identity)
             for (uint32_t q = 0; q < 64; ++q) L[q] = (uint8_t)q;
             continue;
         }
@@ -2531,7 +2532,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             P.init_re = init->re;
             P.init_im = init->im;
         }
-        if (kq < KP) {   // live-tile sweep (in place, identity layout)
+        if (live[kq]) {   // live-tile sweep (in place, identity layout)
             P.flags |= F_LIVE;
             P.lfree = P.lfix = 0;
             if (pending_init) {
@@ -2674,7 +2675,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     }
     if (cur != ctx.psi) throw std::runtime_error("fused planner: layout parity left the state in the scratch buffer");
     // what the buffer may hold from now on: the final support if every sweep was a live one
-    if (track && KP == NLG) {
+    if (track) {   // the support analysis holds whatever the sweeps were
         dfree_ = sup_end;
         dfix_ = (bx_end ^ xmask_) & ~sup_end & all;
     } else {
