@@ -204,3 +204,23 @@ def test_twirl_decoherence_matches_oracle(lib, oracle):
         lib.twirl_decoherence(1.0, 1.0, 3.0)   # T2 > 2 T1
     with pytest.raises(lib.TusqError):
         lib.twirl_decoherence(-1.0, 1.0, 1.0)
+
+
+def test_live_tile_plan(lib):
+    # live tiles: after a reset the planner's support analysis bounds the
+    # tiles a sweep visits -- the same sweeps and gate applications, far fewer bytes; a reset group
+    # moves one tile (64 KiB); a noiseless circuit of diagonal gates after an X-load folds entirely
+    cfg = W.config("C3")
+    nz = cfg.noise
+    t = lib.build_error_tree(cfg.n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
+    _, s = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY)
+    full = 2.0 * (1 << cfg.n) * 16
+    assert s["sweeps"] > 0 and s["hbm_bytes"] < 0.7 * s["sweeps"] * full
+    # one H on a low qubit after a reset: the reset group is one tile, written as one tile
+    n = 20
+    ops = [W.op(W.X, 15), W.op(W.H, 3)]
+    t = lib.build_error_tree(n, ops, 0.0, 0.0, 0.0, 8, 1, prune=False)
+    _, s = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY)
+    assert s["fused_launches"] == 1
+    # the launch moves one 64 KiB tile; finish() writes the zeros outside it once (2^n x 16 B)
+    assert s["hbm_bytes"] <= 4096 * 16 + (1 << n) * 16
