@@ -381,8 +381,14 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     void *scr = nullptr;
     const size_t nslots = std::max<uint64_t>(1, off1 - off0);
     const size_t nblk = 2 * nb + 16;
-    const size_t scr_bytes = (nslots + nblk + htab.size() + 2) * 8;
-    uint64_t *d_slots = nullptr, *d_tab = nullptr;
+    uint64_t maxdraws = 1;   // the most draws one state vector takes (sums-only block lists)
+    for (const SGroup &g : groups) {
+        uint64_t d = 0;
+        for (uint64_t li = g.l0; li < g.l1; ++li) d += t->leaves[li].count;
+        maxdraws = std::max(maxdraws, d);
+    }
+    const size_t scr_bytes = (nslots + nblk + htab.size() + maxdraws + 2) * 8;
+    uint64_t *d_slots = nullptr, *d_tab = nullptr, *d_blist = nullptr;
     double *d_blocks = nullptr;
     uint32_t *d_edges = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -407,7 +413,8 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
         d_slots = (uint64_t *)scr;
         d_blocks = (double *)(d_slots + nslots);
         d_tab = (uint64_t *)(d_blocks + nblk);
-        d_edges = (uint32_t *)(d_tab + htab.size());
+        d_blist = d_tab + htab.size();
+        d_edges = (uint32_t *)(d_blist + maxdraws);
         if (comm) TQ_RUN_CUDA(cudaMemsetAsync(d_slots, 0, nslots * sizeof(uint64_t), st));
         TQ_RUN_CUDA(cudaMemsetAsync(d_edges, 0, sizeof(uint32_t), st));
         if (!htab.empty())
@@ -446,31 +453,49 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
             if (ss != TUSQ_OK) { cleanup(); return ss; }
             groups.clear();
         }
-        for (const SGroup &g : groups) {
+        // transition decisions (reset vs uncompute), made one group AHEAD: a state that the next
+        // transition discards (it resets) need not be stored after sampling (sums-only sweeps)
+        struct Dec { bool reset; Cursor cf, c; InitState init; uint64_t sa_after; };
+        auto decide = [&](size_t gi, uint64_t sa) {
+            const SGroup &g = groups[gi];
+            const Leaf &l = core[g.l0 - lb];
+            const Leaf *prev = g.l0 > lb ? &core[g.l0 - lb - 1] : (cont ? &prev_core : nullptr);
+            Dec d;
+            d.init = InitState{0, 1.0, 0.0};
+            d.cf = fold ? fold_prefix(*t, l, &d.init.index, &d.init.re, &d.init.im) : Cursor{0, 0};
+            d.c = Cursor{0, 0};
+            const uint64_t reset_cost = suffix_len(*t, l, d.cf);
+            d.reset = prev == nullptr;
+            if (!d.reset) {
+                d.c = common_prefix(*t, *prev, l);
+                const uint64_t up = suffix_len(*t, *prev, d.c), down = suffix_len(*t, l, d.c);
+                if ((hybrid && reset_cost < up + down) || sa + up + down > budget) d.reset = true;
+                else d.sa_after = sa + up + down;
+            }
+            if (d.reset) d.sa_after = reset_cost;
+            return d;
+        };
+        Dec next{};
+        for (size_t gi = 0; gi < groups.size(); ++gi) {
+            const SGroup &g = groups[gi];
             // ---- transition to the group's core (uncompute to the divergence slot, then forward)
             const Leaf &l = core[g.l0 - lb];
             const Leaf *prev = g.l0 > lb ? &core[g.l0 - lb - 1] : (cont ? &prev_core : nullptr);
+            const Dec cur = gi == 0 ? decide(0, since_anchor) : next;
+            if (gi + 1 < groups.size()) next = decide(gi + 1, cur.sa_after);
+            const bool next_resets = gi + 1 < groups.size() && next.reset;
             ops.clear();
-            InitState init{0, 1.0, 0.0};
-            Cursor cf = fold ? fold_prefix(*t, l, &init.index, &init.re, &init.im) : Cursor{0, 0};
-            uint64_t reset_cost = suffix_len(*t, l, cf);
-            bool reset = prev == nullptr;
+            InitState init = cur.init;
+            const Cursor cf = cur.cf;
+            bool reset = cur.reset;
             if (!reset) {
-                Cursor c = common_prefix(*t, *prev, l);
-                uint64_t up = suffix_len(*t, *prev, c), down = suffix_len(*t, l, c);
-                if ((hybrid && reset_cost < up + down) || since_anchor + up + down > budget) {
-                    reset = true;
-                } else {
-                    append_inverse(*t, *prev, c, ops);
-                    append_forward(*t, l, c, ops);
-                    since_anchor += up + down;
-                }
-            }
-            if (reset) {
+                append_inverse(*t, *prev, cur.c, ops);
+                append_forward(*t, l, cur.c, ops);
+            } else {
                 stats.resets++;
                 append_forward(*t, l, cf, ops);
-                since_anchor = ops.size();
             }
+            since_anchor = cur.sa_after;
             stats.gate_apps += ops.size();
             // A leaf whose whole executed stream folds (reset with nothing left to apply) is the basis
             // state amp|x>: it stays VIRTUAL -- no device pass -- and its draws are x ^ readout mask
@@ -503,7 +528,7 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
             if (fuse) {
                 // (plan-only runs pass a placeholder pointer: nothing is launched)
                 double *sums_dst = want_sums ? (dry ? reinterpret_cast<double *>(16) : d_blocks) : nullptr;
-                planner.execute_ex(ops, ctx, reset ? &init : nullptr, sums_dst, &sums);
+                planner.execute_ex(ops, ctx, reset ? &init : nullptr, sums_dst, &sums, want_sums && next_resets);
             } else {
                 if (reset) {
                     if (ctx.timer) ctx.timer->begin(st);
@@ -535,6 +560,14 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
                 const Leaf &l0 = t->leaves[g.l0];
                 if (!dry) {
                     launch_scan_blocks(d_blocks, d_blocks + nb, nb, xm >> bb, st);
+                    if (fuse && planner.pending_tiles()) {
+                        // sums-only sweep: find the blocks the draws land in, compute and store
+                        // just those tiles, then draw as usual
+                        launch_draws(psi, n, prec, bb, d_blocks, d_blocks + nb, draws, t->seed, g.l0,
+                                     g.tab ? d_tab + (g.tab - 1) : nullptr, (uint32_t)(g.l1 - g.l0), tmask[g.l0 - lb],
+                                     eps, xm, d_slots + (l0.offset - off0), d_edges, st, d_blist);
+                        planner.replay_tiles(ctx, d_blist, draws, xm >> bb);
+                    }
                     stats.sample_bytes += launch_draws(psi, n, prec, bb, d_blocks, d_blocks + nb, draws, t->seed, g.l0,
                                                        g.tab ? d_tab + (g.tab - 1) : nullptr, (uint32_t)(g.l1 - g.l0),
                                                        tmask[g.l0 - lb], eps, xm, d_slots + (l0.offset - off0), d_edges,

@@ -137,6 +137,9 @@ struct GRec {
 };
 
 enum : uint32_t { F_INIT = 1, F_SUMS = 2, F_SCALE = 4, F_LBASE = 8, F_BULK = 16, F_LIVE = 32, F_VMASK = 64, F_TSTORE = 128,
+                  F_NOSTORE = 256,   // block sums only: the state is not written (the sampler's chosen
+                                     // tiles are recomputed by an F_TLIST launch of the same group)
+                  F_TLIST = 512,     // visit only the tiles tlist[i] ^ tl_xor, i < nlist (device list)
                   F_DBG_NOSTORE = 1u << 31 };   // (debug-knob builds only: skip the stores, for timing)
 constexpr int NCH = 4;             // 8-bit chunks of the tile index (n <= TB + 8 * NCH = 44 fused)
 
@@ -153,6 +156,8 @@ struct Params {
                                   //   init_r of thread init_t of the (single, F_LIVE) tile, 0 elsewhere
     uint64_t lfree, lfix;         // F_LIVE: only the tiles T = pdep(i, lfree) | lfix, i < nlive, can hold
     uint64_t nlive;               //   nonzero amplitudes (support analysis); the rest stay zero
+    const uint64_t *tlist;        // F_TLIST: device list of tile indices (XOR tl_xor), nlist of them
+    uint64_t nlist, tl_xor;
     uint64_t vfree, vfix;         // F_VMASK (read layout = identity): the buffer holds the state only on
                                   //   {x : (x & ~vfree) == vfix}; elsewhere it is zero but not written:
                                   //   tiles outside are not loaded (zeros), elements outside read as 0
@@ -750,6 +755,7 @@ __device__ __forceinline__ uint64_t cta_tile(uint64_t j, const Params &P)
 {
     const uint64_t t = (uint64_t)blockIdx.x * NG + (j % NG) + (j / NG) * ((uint64_t)gridDim.x * NG);
     if (P.flags & F_LIVE) return t < P.nlive ? pdep64(t, P.lfree) | P.lfix : ~0ull;
+    if (P.flags & F_TLIST) return t < P.nlist ? P.tlist[t] ^ P.tl_xor : ~0ull;
     return t < P.ntiles ? t : ~0ull;
 }
 
@@ -893,7 +899,7 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
     for (uint64_t j = grp;; j += NG, base = dep_add(base, P.dstep, P.outer)) {
         const uint64_t T = cta_tile(j, P);
         if (T == ~0ull) break;
-        const bool live = P.flags & F_LIVE;
+        const bool live = P.flags & (F_LIVE | F_TLIST);
         if (live) base = pdep_outer(T, P.outer);   // sparse tile sequence: no incremental bases
         const uint64_t nbase = live ? pdep_outer(cta_tile(j + NBUF, P), P.outer) : dep_add(base, dissue, P.outer);
         V *sm = smbase + (size_t)(j % NBUF) * (1u << TB);
@@ -933,7 +939,8 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                 for (int r = 0; r < NR; ++r) a[r] = *reinterpret_cast<const V *>(smb + (t0 ^ P.ph[0].so[r]));
             }
         }
-        const bool tstore = P.flags & F_TSTORE;   // (the buffer then stays ours until the stores read it)
+        // (the buffer then stays ours until the stores read it)
+        const bool tstore = (P.flags & F_TSTORE) && !(P.flags & F_NOSTORE);
         if (!tstore && (P.last_xpose == 0xFFFFu || dead)) {   // no transpose: release the buffer right away
             if (P.flags & F_BULK) fence_proxy_async();
             named_bar(bar);
@@ -1054,8 +1061,8 @@ __global__ void __launch_bounds__(NT * NG, (NG == 1 ? 2 : 1)) k_fused(const type
                 __trap();
             }
 #endif
-        if (tstore) {
-            // (written above)
+        if (tstore || (P.flags & F_NOSTORE)) {
+            // (written above / not written: block sums only)
         } else if (P.st_pair) {
             switch (P.st_pair) {
 #define TQ_SP(v) case v: if constexpr (v < NR) store_pairs<v>(q0, a, P); break;
@@ -1402,6 +1409,9 @@ struct Built {
 struct tq::PlanScratch {
     Built B;
     uint16_t V[tq::fk::NT][tq::fk::NR], M[1 << tq::fk::TB];   // gather-table simulation
+    tq::fk::Params replay;       // the last group of a sums-only transition (replay_tiles)
+    const void *rsrc = nullptr;
+    void *rdst = nullptr;
 };
 namespace tq {
 
@@ -2157,13 +2167,16 @@ static int blocks_per_sm(int prec)
 
 void FusedPlanner::execute(const std::vector<Op> &ops, Ctx &ctx)
 {
-    execute_ex(ops, ctx, nullptr, nullptr, nullptr);
+    execute_ex(ops, ctx, nullptr, nullptr, nullptr, false);
 }
 
 bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitState *init, double *d_sums,
-                              bool *sums_written)
+                              bool *sums_written, bool sums_only)
 {
     if (sums_written) *sums_written = false;
+    if (pending_tiles_) throw std::runtime_error("fused planner: a sums-only transition was not replayed");
+    if (stale_ && !init) throw std::runtime_error("fused planner: uncompute from a state that was not stored");
+    stale_ = false;
     // strict grouping when it costs (almost) no extra sweeps -- e.g. ripple-carry ladders --
     // otherwise tile membership for controls/diagonals only while there is room (e.g. QFT)
     bool strict = false;
@@ -2559,6 +2572,14 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         const bool last = gi + 1 == groups.size();
         bool want = last && d_sums && B.tile == ((1ull << TB) - 1);
         if (want) P.flags |= F_SUMS;
+        // sums only: the caller discards this state right after sampling it (the next transition
+        // resets), so the last sweep writes only its block sums; the sampler's chosen tiles are
+        // then recomputed and stored by replay_tiles()
+        const bool nostore = want && sums_only && !ctx.dry && !pending_init && !(P.flags & F_LIVE);
+        if (nostore) {
+            P.flags |= F_NOSTORE;
+            P.flags &= ~(uint32_t)F_TSTORE;
+        }
 #ifdef TUSQ_DEBUG_KNOBS   // TUSQ_DBG_NOSTORE=1: the sweeps skip their stores (wrong results; timing only)
         static const bool dbg_nostore = getenv("TUSQ_DBG_NOSTORE") != nullptr;
         if (dbg_nostore) P.flags |= F_DBG_NOSTORE;
@@ -2634,7 +2655,14 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             else
                 k_fused<float><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((const float2 *)src, (float2 *)dst, P,
                                                                           d_sums);
-            if (ctx.timer) ctx.timer->end(ctx.st, bytes, (P.flags & (F_LIVE | F_VMASK | F_INIT)) ? 0 : 2);
+            if (ctx.timer)
+                ctx.timer->end(ctx.st, nostore ? bytes - s : bytes, (P.flags & (F_LIVE | F_VMASK | F_INIT | F_NOSTORE)) ? 0 : 2);
+            if (nostore) {
+                scratch_->replay = P;
+                scratch_->rsrc = src;
+                scratch_->rdst = dst;
+                pending_tiles_ = true;
+            }
 #ifdef TUSQ_DEBUG_KNOBS   // TUSQ_DBG_TRACE=1: one line per K5 launch (group shape), for launch-time fits
             static const bool dbg_trace = getenv("TUSQ_DBG_TRACE") != nullptr;
             if (dbg_trace) {
@@ -2657,11 +2685,14 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             }
 #endif
         }
-        count(ctx, bytes, true);
+        count(ctx, nostore ? (bytes - s) : bytes, true);   // (a sums-only sweep reads, writes nothing)
         pending_init = false;
         // the valid set after this sweep: a live sweep (in place, identity layout) wrote its live
         // tiles whole; any other sweep wrote every tile
-        if (P.flags & F_LIVE) {
+        if (P.flags & F_NOSTORE) {
+            // nothing written: the buffer still holds this group's input (and will be mixed with
+            // the replayed tiles); only a reset may follow (stale_)
+        } else if (P.flags & F_LIVE) {
             uint64_t tpos = 0;
             for (int b = 0; b < TB; ++b) tpos |= bit(P.pin[b]);
             vfree_ = tpos | pdep_mask(P.lfree, P.outer);
@@ -2713,6 +2744,7 @@ void FusedPlanner::close_blocks(Ctx &ctx, uint32_t block_bits)
 
 void FusedPlanner::finish(Ctx &ctx)
 {
+    if (stale_ || pending_tiles_) throw std::runtime_error("fused planner: the call ended on a state that was not stored");
     const uint64_t all = n_ >= 64 ? ~0ull : (1ull << n_) - 1;
     if ((vfree_ & all) == all) return;
     double b = 0;
@@ -2721,6 +2753,30 @@ void FusedPlanner::finish(Ctx &ctx)
     count(ctx, b, false);
     vfree_ = ~0ull;
     vfix_ = 0;
+}
+
+void FusedPlanner::replay_tiles(Ctx &ctx, const uint64_t *d_blist, uint64_t n, uint64_t mh)
+{
+    if (!pending_tiles_) return;
+    pending_tiles_ = false;
+    stale_ = true;   // the buffer now mixes the group's input and the replayed tiles
+    if (!n) return;
+    Params &P = scratch_->replay;
+    P.flags = (P.flags & ~(uint32_t)(F_NOSTORE | F_SUMS | F_LIVE | F_TSTORE)) | F_TLIST;
+    P.tlist = d_blist;
+    P.nlist = n;
+    P.tl_xor = mh ^ (P.xout >> TB);   // logical block b of the sampler -> tile index (tile {0..11})
+    const uint64_t grid = std::min<uint64_t>((n + NG - 1) / NG, (uint64_t)device_sm_count() * blocks_per_sm(prec_));
+    const size_t smem = smem_bytes(prec_);
+    if (prec_ == 128)
+        k_fused<double><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((const double2 *)scratch_->rsrc,
+                                                                   (double2 *)scratch_->rdst, P, nullptr);
+    else
+        k_fused<float><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((const float2 *)scratch_->rsrc,
+                                                                  (float2 *)scratch_->rdst, P, nullptr);
+    ctx.stats->launches++;
+    ctx.stats->fused_launches++;
+    ctx.stats->hbm_bytes += 2.0 * (double)n * (double)(1u << TB) * (prec_ == 128 ? 16 : 8);
 }
 
 }  // namespace tq

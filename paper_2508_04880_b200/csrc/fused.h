@@ -59,8 +59,15 @@ public:
     void execute(const std::vector<Op> &ops, Ctx &ctx);
     // init: the state is first reset to init (no load); d_sums: if the last sweep's tile is the
     // contiguous block {0..11}, it writes per-block |amp|^2 sums (physical block order) there.
+    // sums_only: the caller samples this state and then discards it (the next transition resets):
+    // the last sweep writes only the block sums (if it produces them) and replay_tiles() then
+    // computes and stores just the tiles the sampler's draws land in
     bool execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitState *init, double *d_sums,
-                    bool *sums_written);
+                    bool *sums_written, bool sums_only = false);
+    bool pending_tiles() const { return pending_tiles_; }
+    // d_blist: n logical block indices (the sampler's chosen blocks, repeats allowed); mh: the
+    // sampler's physical-block XOR (xmask() >> 12)
+    void replay_tiles(Ctx &ctx, const uint64_t *d_blist, uint64_t n, uint64_t mh);
     // the logical state may be stored XOR-relabelled; materialize() clears the mask
     uint64_t xmask() const { return xmask_; }
     // a second device buffer of the state's size: enables the layout-changing (out-of-place) sweeps
@@ -78,7 +85,7 @@ public:
     void reset_mask() { xmask_ = 0; }
     // the caller wrote the basis state |index> (K7) into the state: the known support is one element
     // and the whole buffer is valid
-    void note_basis(uint64_t index) { xmask_ = 0; dfree_ = 0; dfix_ = index; vfree_ = ~0ull; vfix_ = 0; }
+    void note_basis(uint64_t index) { xmask_ = 0; dfree_ = 0; dfix_ = index; vfree_ = ~0ull; vfix_ = 0; stale_ = false; }
     // The buffer may hold the state only on a valid set V = {x : (x & ~vfree) == vfix} (physical,
     // identity layout; outside it the state is zero and the buffer stale).  Readers outside K5:
     // close_blocks() makes V a union of whole 2^12-element blocks (zeros written inside the blocks
@@ -98,6 +105,7 @@ private:
     // amplitude has (index & ~dfree_) == dfix_; dfree_ = ~0 when unknown
     uint64_t dfree_ = ~0ull, dfix_ = 0;
     uint64_t vfree_ = ~0ull, vfix_ = 0;   // the valid set V (see valid_set)
+    bool pending_tiles_ = false, stale_ = false;
     void *alt_ = nullptr;
     uint64_t alt_lazy_ = 0;
     bool alt_owned_ = false;

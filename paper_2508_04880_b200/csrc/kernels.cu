@@ -511,7 +511,8 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
                                                uint64_t leaf, const uint64_t *__restrict__ ltab, uint32_t nlt,
                                                uint64_t omask, double edge_eps, uint64_t xm,
                                                uint64_t *__restrict__ out, uint32_t *__restrict__ edges,
-                                               double tg_total, double tg_lo, double tg_hi, uint64_t ohi)
+                                               double tg_total, double tg_lo, double tg_hi, uint64_t ohi,
+                                               uint64_t *__restrict__ blist)
 {
     // Leaves that share one state vector (they differ only in terminal X flips, DESIGN reading #7:
     // measurement noise relabels the drawn bitstring) are drawn in ONE launch: ltab holds
@@ -587,6 +588,10 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
     }
     b = __shfl_sync(0xffffffffu, b, bl);
     bbase = __shfl_sync(0xffffffffu, bbase, bl);
+    if (blist) {   // blocks-only pass: the block this draw lands in (K5 then computes those tiles)
+        if (lane == 0) blist[warp] = b;
+        return;
+    }
     const uint64_t bs = 1ull << block_bits;
     const uint64_t chunk = (bs + 31) / 32;
     const uint64_t c0 = lane * chunk < bs ? lane * chunk : bs, c1 = c0 + chunk < bs ? c0 + chunk : bs;
@@ -648,7 +653,7 @@ __global__ void __launch_bounds__(TPB) k_draws(const typename CV<R>::T *__restri
 double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
                     const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, const uint64_t *d_ltab,
                     uint32_t nlt, uint64_t omask, double edge_eps, uint64_t xm, uint64_t *d_out, uint32_t *d_edges,
-                    cudaStream_t st)
+                    cudaStream_t st, uint64_t *d_blist)
 {
     if (!n_draws) return 0.0;
     uint64_t nb = 1ull << (n - block_bits);
@@ -656,11 +661,12 @@ double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, 
     uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
     if (prec == 64)
         k_draws<float><<<grid, TPB, 0, st>>>((const float2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0, k1,
-                                             leaf, d_ltab, nlt, omask, edge_eps, xm, d_out, d_edges, 0.0, 0.0, 0.0, 0);
+                                             leaf, d_ltab, nlt, omask, edge_eps, xm, d_out, d_edges, 0.0, 0.0, 0.0, 0,
+                                             d_blist);
     else
         k_draws<double><<<grid, TPB, 0, st>>>((const double2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0,
                                               k1, leaf, d_ltab, nlt, omask, edge_eps, xm, d_out, d_edges, 0.0, 0.0, 0.0,
-                                              0);
+                                              0, d_blist);
     return (double)n_draws * (double)(1ull << block_bits) * (prec == 64 ? 8.0 : 16.0);
 }
 
@@ -677,11 +683,11 @@ double launch_draws_window(const void *psi, uint32_t n, int prec, uint32_t block
     if (prec == 64)
         k_draws<float><<<grid, TPB, 0, st>>>((const float2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0, k1,
                                              leaf, nullptr, 0, omask, edge_eps, 0, d_out, d_edges, t_total, t_lo, t_hi,
-                                             ohi);
+                                             ohi, nullptr);
     else
         k_draws<double><<<grid, TPB, 0, st>>>((const double2 *)psi, block_bits, d_phys, d_sprefix, nb, n_draws, k0,
                                               k1, leaf, nullptr, 0, omask, edge_eps, 0, d_out, d_edges, t_total, t_lo,
-                                              t_hi, ohi);
+                                              t_hi, ohi, nullptr);
     return (double)n_draws * (double)(1ull << block_bits) * (prec == 64 ? 8.0 : 16.0);
 }
 

@@ -32,7 +32,7 @@ void launch_scan_blocks(const double *d_phys, double *d_prefix, uint64_t nb, uin
 double launch_draws(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
                     const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, const uint64_t *d_ltab,
                     uint32_t nlt, uint64_t omask, double edge_eps, uint64_t xm, uint64_t *d_out, uint32_t *d_edges,
-                    cudaStream_t st);
+                    cudaStream_t st, uint64_t *d_blist = nullptr);   // d_blist: only write each draw's block
 // sharded mode: the draws of one leaf that fall into this shard's CDF window [t_lo, t_hi)
 double launch_draws_window(const void *psi, uint32_t n, int prec, uint32_t block_bits, const double *d_phys,
                            const double *d_sprefix, uint64_t n_draws, uint64_t seed, uint64_t leaf, uint64_t omask,
