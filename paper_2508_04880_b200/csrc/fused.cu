@@ -2579,6 +2579,19 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         if (nostore) {
             P.flags |= F_NOSTORE;
             P.flags &= ~(uint32_t)F_TSTORE;
+            if (P.flags & F_VMASK) {
+                // nothing is written, so only the tiles V touches need a visit (the other block sums
+                // are zero): a live sweep over V's tiles (T = physical outer bits ^ xin)
+                P.lfree = P.lfix = 0;
+                uint32_t j = 0;
+                for (uint64_t m = P.outer; m; m &= m - 1, ++j) {
+                    const uint32_t pos = (uint32_t)__builtin_ctzll(m);
+                    if ((P.vfree >> pos) & 1) P.lfree |= 1ull << j;
+                    else P.lfix |= (((P.vfix ^ P.xin) >> pos) & 1ull) << j;
+                }
+                P.nlive = 1ull << __builtin_popcountll(P.lfree);
+                P.flags |= F_LIVE;
+            }
         }
 #ifdef TUSQ_DEBUG_KNOBS   // TUSQ_DBG_NOSTORE=1: the sweeps skip their stores (wrong results; timing only)
         static const bool dbg_nostore = getenv("TUSQ_DBG_NOSTORE") != nullptr;
@@ -2646,10 +2659,18 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             // nlive = 1); the rest of the buffer is not written -- the valid set V shrinks to that
             // tile (the zeros outside V are only written by finish(), once per call).
             // live-tile sweeps write the sums of their live tiles only: the others are zero
-            if ((P.flags & F_LIVE) && want &&
+            if ((P.flags & F_LIVE) && want && !(nostore && src == dst) &&
                 cudaMemsetAsync(d_sums, 0, (size_t)P.ntiles * sizeof(double), ctx.st) != cudaSuccess)
                 throw std::runtime_error("cudaMemsetAsync (block sums) failed");
-            if (prec_ == 128)
+            if (nostore && src == dst) {
+                // The group's gates act inside tiles, and tile {0..11} is the sampler's block: each
+                // block's |amp|^2 sum is the same before and after the group (a unitary on the
+                // block; outer qubits enter only as controls).  In place and in the identity
+                // layout the block keeps its physical index, so the sums are those of the INPUT:
+                // one read of the valid set, no K5 sweep (its chosen tiles are replayed later).
+                const uint64_t vf = (P.flags & F_VMASK) ? P.vfree : ~0ull, vx = (P.flags & F_VMASK) ? P.vfix : 0;
+                launch_block_sums(src, n_, prec_, TB, d_sums, ctx.st, vf, vx);
+            } else if (prec_ == 128)
                 k_fused<double><<<(unsigned)grid, NT * NG, smem, ctx.st>>>((const double2 *)src, (double2 *)dst, P,
                                                                            d_sums);
             else
@@ -2678,9 +2699,9 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
                 }
                 int contig = 1;
                 for (int b = 0; b < TB; ++b) contig &= P.pin[b] == b;
-                fprintf(stderr, "[k5] idx %d ops %zu recs %u ph %u init %d contig %d oop %d gtab %d nlive %llu vmask %d tile %#llx H %d DK %d CX %d D %d XP %d XY %d TP %d O %d CU %d CCX %d\n",
+                fprintf(stderr, "[k5] idx %d ops %zu recs %u ph %u init %d contig %d oop %d gtab %d nlive %llu vmask %d ns %d tile %#llx H %d DK %d CX %d D %d XP %d XY %d TP %d O %d CU %d CCX %d\n",
                         ctx.timer ? (int)ctx.timer->pending() - 1 : -1, G.ops.size(), P.ngate, P.nphase, pending_init ? 1 : 0, contig, src != dst ? 1 : 0,
-                        P.gtab != 0xFFFFu, (unsigned long long)((P.flags & F_LIVE) ? P.nlive : P.ntiles), (P.flags & F_VMASK) ? 1 : 0, (unsigned long long)B.tile, cnt[0], cnt[1], cnt[2], cnt[3], cnt[4], cnt[5],
+                        P.gtab != 0xFFFFu, (unsigned long long)((P.flags & F_LIVE) ? P.nlive : P.ntiles), (P.flags & F_VMASK) ? 1 : 0, (P.flags & F_NOSTORE) ? 1 : 0, (unsigned long long)B.tile, cnt[0], cnt[1], cnt[2], cnt[3], cnt[4], cnt[5],
                         cnt[6], cnt[7], cnt[8], cnt[9]);
             }
 #endif

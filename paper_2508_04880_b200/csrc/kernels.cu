@@ -392,17 +392,27 @@ __global__ void __launch_bounds__(TPB) k_block_sums(const typename CV<R>::T *__r
     using V = typename CV<R>::T;
     const uint64_t bs = 1ull << block_bits;
     const uint64_t base = (uint64_t)blockIdx.x * bs;
-    // a block outside the valid set holds no amplitude (K5 live tiles: the buffer is stale there;
-    // the valid set covers whole blocks when the sampler runs, FusedPlanner::close_blocks)
+    // a block outside the valid set holds no amplitude (K5 live tiles: the buffer is stale there);
+    // inside a block, positions the valid set fixes mask the elements (read as zero, not loaded)
     if ((base ^ vfix) & ~vfree & ~(bs - 1)) {
         if (threadIdx.x == 0) out[blockIdx.x] = 0.0;
         return;
     }
     double acc = 0.0;
+    const uint64_t lowfix = ~vfree & (bs - 1);   // in-block positions the valid set fixes
     if constexpr (PER > 0) {
         V a[PER];
+        if (lowfix) {   // elements outside the valid set read as zero (and are not loaded)
 #pragma unroll
-        for (int k = 0; k < PER; ++k) a[k] = __ldcs(psi + base + threadIdx.x + k * TPB);
+            for (int k = 0; k < PER; ++k) {
+                const uint64_t x = base + threadIdx.x + k * TPB;
+                if (((x ^ vfix) & lowfix) == 0) a[k] = __ldcs(psi + x);
+                else { a[k].x = 0; a[k].y = 0; }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < PER; ++k) a[k] = __ldcs(psi + base + threadIdx.x + k * TPB);
+        }
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const double re = a[k].x, im = a[k].y;
@@ -410,6 +420,7 @@ __global__ void __launch_bounds__(TPB) k_block_sums(const typename CV<R>::T *__r
         }
     } else {
         for (uint64_t i = threadIdx.x; i < bs; i += blockDim.x) {
+            if (((base + i) ^ vfix) & lowfix) continue;
             V a = psi[base + i];
             double re = a.x, im = a.y;
             acc += re * re + im * im;

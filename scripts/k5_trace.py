@@ -74,6 +74,6 @@ if __name__ == "__main__":
                                      ("recs", "ph", "XP", "H", "DK", "CX", "D", "CU", "CCX", "TP", "XY", "oop",
                                       "contig", "gtab")} if rows else None,
                      "rows": [[r["ms"], r["recs"], r["XP"], r["H"], r["DK"], r["CX"], r["CU"], r["CCX"], r["XY"],
-                               r["oop"], r["contig"], r["init"], r["gtab"], r["nlive"], r["vmask"]] for r in rows]}
+                               r["oop"], r["contig"], r["init"], r["gtab"], r["nlive"], r["vmask"], r["ns"]] for r in rows]}
         print(name, json.dumps({k: v for k, v in out[name].items() if k != "rows"}), flush=True)
     json.dump(out, open(os.path.join(ROOT, "gpurun_out", "k5_trace.json"), "w"), indent=1)
