@@ -130,8 +130,9 @@ def cpu_oracle_rate(cfg, max_seconds: float = 20.0):
 
 
 def ncu_traffic(prec):
-    """DRAM bytes per k_fused launch from the committed in-bench ncu --set full capture (c128)."""
-    for name in ("r2_ncu_k_fused_in_bench.json", "r1_ncu_k_fused_in_bench.json"):
+    """DRAM bytes of one DENSE k_fused sweep (2 x 2^30 x 16 B algorithmic) from the committed
+    ncu --set full capture (c128): traffic ~= algorithmic means no wasted re-reads."""
+    for name in ("r2_ncu_k_fused_dense.json", "r1_ncu_k_fused_in_bench.json"):
         path = os.path.join(ROOT, "profiles", name)
         if prec != 128 or not os.path.exists(path):
             continue
@@ -195,8 +196,8 @@ def main():
     ap.add_argument("--no-fuse", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-leaves", type=int, default=48,
-                    help="leaves per batch of the untimed per-launch profile pass (3 batches)")
+    ap.add_argument("--profile-leaves", type=int, default=100,
+                    help="leaves per slice of the untimed per-launch profile pass (8 slices spread over the range)")
     ap.add_argument("--mode", default="replica", choices=["replica", "sharded"],
                     help="sharded: amplitudes split over the N ranks by global qubits (e.g. --config C5 on 8 GPUs)")
     ap.add_argument("--shards", type=int, default=0,
@@ -277,10 +278,11 @@ def main():
     value, wall_max, t_dev_max, t_red_max = [float(x) for x in vals.cpu()]
     info = tree.info()
 
-    # ---- untimed profile pass: per-launch CUDA events over 3 short batches spread over the range
+    # ---- untimed profile pass: per-launch CUDA events over 8 slices spread evenly over the range
+    # (slices of ~100 leaves: the per-call fixed work stays ~1 % of a slice's device time)
     lb, le = batches[0][0], batches[-1][1]
     prof = []
-    for frac in (0.1, 0.5, 0.85):
+    for frac in [(i + 0.5) / 8 for i in range(8)]:
         b = lb + int((le - lb) * frac)
         e = min(le, b + args.profile_leaves)
         if e > b:
@@ -312,8 +314,9 @@ def main():
                    "note": "traversal/sampling = device_s x the gate/sampler kernel shares of the profile pass"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
-                     "traffic_source": (f"dram__bytes_read.sum + dram__bytes_write.sum of one k_fused launch of this "
-                                        f"bench under ncu --set full ({traffic_src})") if traffic_src else None,
+                     "traffic_source": (f"dram__bytes_read.sum + dram__bytes_write.sum of one dense k_fused sweep "
+                                        f"(algorithmic 2 x 2^n x 16 B) under ncu --set full ({traffic_src})")
+                     if traffic_src else None,
                      "kernel": "k_fused (K5)" if not args.no_fuse else "K1-K4",
                      "per_unit": ("one fused sweep = 2 x 2^n x 16 B over every tile it visits: a live-tile sweep "
                                   "(after a reset) moves 2 x its live tiles x 64 KiB, a reset sweep writes one tile, "
