@@ -2538,7 +2538,13 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             if (dbg_ts) ts_min = dbg_ts;
 #endif
             // (not on a partly valid buffer: its mostly-zero tiles measured slower with it)
-            if (P.ts_l0 >= ts_min && (vfree_ & all) == all) P.flags |= F_TSTORE;
+            // and only when lanes 0-2 of the last phase carry write-order bits 0-2: the write-order
+            // staging is linear (the bulk copies need contiguous runs), so each quarter warp must
+            // cover one 128-byte row -- otherwise every STS is 8-way bank conflicted (ncu on a
+            // dense C4 sweep: 14 wavefronts per STS, 1.0 G conflicts, ~3 ms of a 15.9 ms sweep)
+            const Phase &lp = P.ph[P.nphase - 1];
+            const uint32_t lane_w = (1u << P.wpos[lp.tl[0]]) | (1u << P.wpos[lp.tl[1]]) | (1u << P.wpos[lp.tl[2]]);
+            if (P.ts_l0 >= ts_min && (vfree_ & all) == all && lane_w == 7u) P.flags |= F_TSTORE;
         }
         if (pending_init) {
             P.flags |= F_INIT;
