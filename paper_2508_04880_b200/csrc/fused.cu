@@ -2804,6 +2804,10 @@ void FusedPlanner::replay_tiles(Ctx &ctx, const uint64_t *d_blist, uint64_t n, u
     ctx.stats->launches++;
     ctx.stats->fused_launches++;
     ctx.stats->hbm_bytes += 2.0 * (double)n * (double)(1u << TB) * (prec_ == 128 ? 16 : 8);
+#ifdef TUSQ_DEBUG_KNOBS   // keep the launch trace aligned with the k_fused launch sequence
+    static const bool dbg_trace = getenv("TUSQ_DBG_TRACE") != nullptr;
+    if (dbg_trace) fprintf(stderr, "[k5r] replay %llu tiles\n", (unsigned long long)n);
+#endif
 }
 
 }  // namespace tq

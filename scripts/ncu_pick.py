@@ -2,7 +2,7 @@
 """Profile one K5 launch of a chosen kind in a C4 leaf batch: the debug-knob build's launch trace
 (TUSQ_DBG_TRACE) finds the index of the first launch matching the kind, then ncu --set full
 captures that k_fused launch from the release build.
-usage: ncu_pick.py KIND OUT [begin count]   KIND: vmask | live | full | init"""
+usage: ncu_pick.py KIND OUT [begin count]   KIND: vmask | live | full | heavy | init"""
 import os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 kind, out = sys.argv[1], sys.argv[2]
@@ -11,11 +11,18 @@ env = dict(os.environ, TUSQ_LIB_NAME="libtusq_dbg.so", TUSQ_DBG_TRACE="1")
 p = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "c4_batch.py"), b, k], env=env, capture_output=True,
                    text=True)
 idx = None
-for i, line in enumerate(l for l in p.stderr.splitlines() if l.startswith("[k5]")):
+i = -1
+for line in (l for l in p.stderr.splitlines() if l.startswith("[k5")):
+    if line.startswith("[k5r]"):   # a replay launch (sums-only sampling): counted, never picked
+        i += 1
+        continue
     kv = line.split()[1:]
     d = {kv[j]: kv[j + 1] for j in range(0, len(kv) - 1, 2)}
+    if d.get("ns") == "1" and d.get("oop") == "0":   # sums from K6 block sums: no k_fused launch
+        continue
+    i += 1
     full = int(d["nlive"]) == (1 << 18)
-    match = {"vmask": full and d["vmask"] == "1", "live": not full and d["init"] == "0", "init": d["init"] == "1",
+    match = {"heavy": full and int(d["recs"]) >= 15 and d.get("ns") == "0", "vmask": full and d["vmask"] == "1", "live": not full and d["init"] == "0", "init": d["init"] == "1",
              "full": full and d["vmask"] == "0"}[kind]
     if match:
         idx = i
