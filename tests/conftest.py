@@ -38,10 +38,11 @@ class _OracleRuns:
             self.runs[name] = self.tree(name).run()
         return self.runs[name]
 
-    def sparse_run(self, name):
+    def sparse_run(self, name, eps=1e-9):
         """Full-run slots of an Adder config from the oracle's sparse replay (oracle/sparse.py,
-        pinned to the dense oracle): each leaf's core replayed, sampled, XORed with its readout mask."""
-        key = ("sparse", name)
+        pinned to the dense oracle): each leaf's core replayed, sampled, XORed with its readout mask;
+        eps = the edge-draw window (1e-9 for c128, 1e-5 for c64, DESIGN reading #17)."""
+        key = ("sparse", name, eps)
         if key not in self.runs:
             import numpy as np
             from oracle import sparse as SP
@@ -53,7 +54,7 @@ class _OracleRuns:
             for l in range(ot.n_leaves):
                 tr, cnt, off = ot.leaf(l)
                 psi = SP.replay(cfg.ops, SP.core_triples(tr, len(cfg.ops)), drop_below=1e-14)
-                k, e = SP.sample(psi, cfg.seed, l, cnt, 1e-9, ot.terminal_mask(l))
+                k, e = SP.sample(psi, cfg.seed, l, cnt, eps, ot.terminal_mask(l))
                 ref[off:off + cnt], edge[off:off + cnt] = k, e
             self.runs[key] = (ref, edge)
         return self.runs[key]

@@ -308,6 +308,17 @@ def test_c3_all_slots(T, torch, oracle_runs):
     assert stats["draws"] == cfg.shots
 
 
+def test_c3_all_slots_c64(T, torch, oracle_runs):
+    # the same at complex64 (fp64 CDF sums; edge window 1e-5, reading #17): exercises the c64 K5
+    # path with live tiles, valid sets and sums-only sampling (replayed tiles) at 24 qubits
+    cfg = W.config("C3")
+    t = _tree(T, cfg)
+    slots, stats = T.run_tree(t, 64)
+    ref, edge = oracle_runs.sparse_run("C3", 1e-5)
+    _check_slots(slots, ref, edge, cfg.shots)
+    assert stats["draws"] == cfg.shots
+
+
 def test_c4_spot_leaves(T, torch, oracle_runs):
     # C4 (30 qubits, 16 GiB c128) in bench's launch configuration (fused, hybrid re-anchor):
     # SURVEY 8(d)'s 9 spot-check leaves (all-I, first 2, last 2, 4 seeded) plus the 2 leaves of
