@@ -255,12 +255,16 @@ def main():
         w0 = time.perf_counter()
         tree = T.build_error_tree(n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
         t_ecm = time.perf_counter() - w0
+        # world * K cost-balanced chunks in DFS order; rank r takes chunks r, r + world, ... (interleaved:
+        # the partition balances gate applications, while device time follows the full sweeps, which
+        # cluster in DFS order -- interleaving spreads them over the ranks).  One rank: contiguous.
         bounds = tree.partition(world * K, prec)
-        batches = [(int(bounds[rank * K + s]), int(bounds[rank * K + s + 1])) for s in range(K)]
+        batches = [(int(bounds[s * world + rank]), int(bounds[s * world + rank + 1])) for s in range(K)]
         ev[0].record(stream)
         for s, (b, e) in enumerate(batches):
+            cont = s > 0 and batches[s - 1][1] == b   # continue the DFS state only across contiguous batches
             _, st = T.run_tree(tree, prec, d_state=state, stream=stream, leaf_begin=b, leaf_end=e,
-                               flags=flags | (T.EXEC_CONTINUE if s else 0), out_slots=slots)
+                               flags=flags | (T.EXEC_CONTINUE if cont else 0), out_slots=slots)
             stats.append(st)
         ev[1].record(stream)
         if comm is not None:
@@ -339,7 +343,7 @@ def main():
                   "gate_apps": int(tot["gate_apps"]), "sweeps": int(tot["sweeps"]),
                   "fused_launches": int(tot["fused_launches"]), "hbm_GB": tot["hbm_bytes"] / 1e9,
                   "tree_leaves": info["n_leaves"], "dftt_ops": info["dftt_ops"], "naive_ops": info["naive_ops"],
-                  "rank_leaves": [lb, le]},
+                  "rank_leaves": int(sum(e - b for b, e in batches))},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         per, cores, desc = cpu_oracle_rate(cfg, args.cpu_seconds)
