@@ -94,7 +94,7 @@ def config_dict(cfg, prec, world):
     """The config both arms report (identical keys and values for the same workload)."""
     return {"workload": workload_desc(cfg), "precision": f"c{prec}", "shots": cfg.shots,
             "l2": f"state {(16 if prec == 128 else 8) * 2 ** cfg.n / 2 ** 30:.0f} GiB >> 126 MB L2 (no flush needed)",
-            "parallelism": f"replica x{world}, contiguous cost-balanced DFS leaf ranges"}
+            "parallelism": f"replica x{world}, cost-balanced DFS leaf chunks (interleaved over the ranks)"}
 
 
 def cpu_oracle_rate(cfg, max_seconds: float = 20.0):
@@ -194,6 +194,8 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--precision", type=int, default=128, choices=[128, 64])
     ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--no-live", action="store_true",
+                    help="plain dense path: no live tiles / valid sets / sums-only sampling (TUSQ_EXEC_NO_LIVE)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-leaves", type=int, default=100,
@@ -230,7 +232,7 @@ def main():
     n = cfg.n
     prec = args.precision
     K = max(1, args.steps)
-    flags = T.EXEC_NO_FUSE if args.no_fuse else 0
+    flags = (T.EXEC_NO_FUSE if args.no_fuse else 0) | (T.EXEC_NO_LIVE if args.no_live else 0)
     dt = torch.complex128 if prec == 128 else torch.complex64
     state = torch.empty(1 << n, dtype=dt, device="cuda")
     stream = torch.cuda.current_stream()
@@ -345,6 +347,8 @@ def main():
                   "tree_leaves": info["n_leaves"], "dftt_ops": info["dftt_ops"], "naive_ops": info["naive_ops"],
                   "rank_leaves": int(sum(e - b for b, e in batches))},
     }
+    line["path"] = ("dense state-vector path (TUSQ_EXEC_NO_LIVE: every sweep visits the whole state)" if args.no_live
+                    else "live tiles + valid sets + sums-only sampling (DESIGN.md)")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         per, cores, desc = cpu_oracle_rate(cfg, args.cpu_seconds)
         line["cpu_baseline"] = {"value": per * info["naive_ops"], "unit": "s", "cores": cores, "kind": "oracle",

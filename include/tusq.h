@@ -126,6 +126,10 @@ typedef struct {
 #define TUSQ_EXEC_CONTINUE    0x40u /* d_state already holds the final state of leaf leaf_begin-1 (left by a
                                        previous call): continue the DFS from there instead of re-anchoring
                                        (a hint: the small-n batched path re-anchors every sub-range) */
+#define TUSQ_EXEC_NO_LIVE     0x100u /* no live tiles / valid sets / sums-only sampling: after a re-anchor
+                                         every fused sweep visits the whole state (the zeros are written
+                                         by the reset), and every sampled state is stored -- the plain
+                                         dense state-vector path, for A/B comparison */
 #define TUSQ_EXEC_NO_BATCH    0x80u /* n <= 13 (c128) / 14 (c64): do not run the batched on-chip path (one
                                        launch, one DFS sub-range per CTA, state in shared memory) but one
                                        transition at a time like larger n */

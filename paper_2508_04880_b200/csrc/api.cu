@@ -426,6 +426,7 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
     const uint64_t budget = ex->reanchor_budget ? ex->reanchor_budget : (prec == 128 ? 1000000ull : 20000ull);
     const double eps = ex->edge_eps > 0 ? ex->edge_eps : (prec == 128 ? 1e-9 : 1e-5);
     FusedPlanner planner(n, prec);
+    planner.set_live(!(ex->flags & TUSQ_EXEC_NO_LIVE));
     const bool fuse = !(ex->flags & TUSQ_EXEC_NO_FUSE) && planner.enabled();
     // small n: the whole range in ONE launch, one sub-range per CTA, state on chip (smallsim.cu)
     const bool small = !(ex->flags & (TUSQ_EXEC_NO_FUSE | TUSQ_EXEC_NO_BATCH)) && n <= small_max_qubits(prec);

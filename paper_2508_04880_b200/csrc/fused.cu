@@ -2255,7 +2255,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
     const uint64_t all = n_ >= 64 ? ~0ull : (1ull << n_) - 1;
     std::vector<uint64_t> supS(NLG, ~0ull), supB(NLG, 0);
     std::vector<char> live(NLG, 0);   // launched group k visits only its live tiles (in place)
-    const bool track = pending_init || (dfree_ & all) != all;
+    const bool track = live_ && (pending_init || (dfree_ & all) != all);
     uint64_t sup_end = all, bx_end = 0;
     if (track) {
         uint64_t sup = pending_init ? 0 : dfree_ & all;   // qubits that may vary
@@ -2289,6 +2289,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         for (size_t g = 0; g < NLG; ++g)
             live[g] = __builtin_popcountll(supS[g] & ~tiles[g] & all) + 3 <= (int)(n_ - TB) || (g == 0 && pending_init);
     }
+    if (!track && pending_init && NLG) live[0] = 1;   // the reset group is always one tile
     std::vector<std::array<uint8_t, 64>> lay(NLG + 1);
 #ifdef TUSQ_DEBUG_KNOBS   // debug builds only: TUSQ_DBG_IDENTITY=1 keeps every layout the identity
     static const bool dbg_identity = getenv("TUSQ_DBG_IDENTITY") != nullptr;
@@ -2581,7 +2582,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         // sums only: the caller discards this state right after sampling it (the next transition
         // resets), so the last sweep writes only its block sums; the sampler's chosen tiles are
         // then recomputed and stored by replay_tiles()
-        const bool nostore = want && sums_only && !ctx.dry && !pending_init && !(P.flags & F_LIVE);
+        const bool nostore = live_ && want && sums_only && !ctx.dry && !pending_init && !(P.flags & F_LIVE);
         if (nostore) {
             P.flags |= F_NOSTORE;
             P.flags &= ~(uint32_t)F_TSTORE;
@@ -2622,7 +2623,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         // bytes: a reset sweep writes one tile; live sweeps move their tiles; a full sweep on a
         // partly valid buffer reads only the tiles V touches
         double bytes = 2 * s;
-        if (pending_init) bytes = tbytes;
+        if (pending_init) bytes = live_ ? tbytes : s;
         else if (P.flags & F_LIVE) bytes = 2.0 * (double)P.nlive * tbytes;
         else if (vmask) bytes = s + (double)(1ull << __builtin_popcountll(P.vfree)) * (prec_ == 128 ? 16 : 8);
         if (!ctx.dry) {
@@ -2663,7 +2664,9 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
             if (ctx.timer) ctx.timer->begin(ctx.st);
             // A reset sweep is ONE CTA computing the tile that holds the basis state (F_LIVE,
             // nlive = 1); the rest of the buffer is not written -- the valid set V shrinks to that
-            // tile (the zeros outside V are only written by finish(), once per call).
+            // tile (the zeros outside V are only written by finish(), once per call).  Without
+            // live tiles (TUSQ_EXEC_NO_LIVE) K7 writes the zeros first and V stays everything.
+            if (pending_init && !live_) launch_init_basis(dst, n_, prec_, 0, 0.0, 0.0, ctx.st);
             // live-tile sweeps write the sums of their live tiles only: the others are zero
             if ((P.flags & F_LIVE) && want && !(nostore && src == dst) &&
                 cudaMemsetAsync(d_sums, 0, (size_t)P.ntiles * sizeof(double), ctx.st) != cudaSuccess)
@@ -2719,7 +2722,7 @@ bool FusedPlanner::execute_ex(const std::vector<Op> &ops, Ctx &ctx, const InitSt
         if (P.flags & F_NOSTORE) {
             // nothing written: the buffer still holds this group's input (and will be mixed with
             // the replayed tiles); only a reset may follow (stale_)
-        } else if (P.flags & F_LIVE) {
+        } else if ((P.flags & F_LIVE) && live_) {
             uint64_t tpos = 0;
             for (int b = 0; b < TB; ++b) tpos |= bit(P.pin[b]);
             vfree_ = tpos | pdep_mask(P.lfree, P.outer);

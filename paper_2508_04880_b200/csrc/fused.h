@@ -75,6 +75,8 @@ public:
     void set_alt(void *alt) { alt_ = alt; }
     // or: allocate it (stream-ordered, `bytes`) only when a call has >= 2 groups; release() frees it
     void set_alt_lazy(uint64_t bytes) { alt_lazy_ = bytes; }
+    // live tiles / valid sets off (TUSQ_EXEC_NO_LIVE): every sweep visits the whole state
+    void set_live(bool on) { live_ = on; }
     void release(cudaStream_t st)
     {
         if (alt_owned_ && alt_) cudaFreeAsync(alt_, st);
@@ -105,7 +107,7 @@ private:
     // amplitude has (index & ~dfree_) == dfix_; dfree_ = ~0 when unknown
     uint64_t dfree_ = ~0ull, dfix_ = 0;
     uint64_t vfree_ = ~0ull, vfix_ = 0;   // the valid set V (see valid_set)
-    bool pending_tiles_ = false, stale_ = false;
+    bool pending_tiles_ = false, stale_ = false, live_ = true;
     void *alt_ = nullptr;
     uint64_t alt_lazy_ = 0;
     bool alt_owned_ = false;

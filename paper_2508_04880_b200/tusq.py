@@ -19,7 +19,7 @@ _lib = C.CDLL(LIB_PATH)
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_OOM, ERR_CUDA, ERR_NCCL, ERR_CAPACITY, ERR_INTERNAL = range(8)
 EXEC_NO_FUSE, EXEC_NO_RESET, EXEC_NO_SAMPLE, EXEC_NO_FOLD, EXEC_PLAN_ONLY, EXEC_PROFILE = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
-EXEC_CONTINUE, EXEC_NO_BATCH = 0x40, 0x80
+EXEC_CONTINUE, EXEC_NO_BATCH, EXEC_NO_LIVE = 0x40, 0x80, 0x100
 APPLY_INVERSE, APPLY_UNFUSED, APPLY_PLAN_ONLY = 0x1, 0x2, 0x4
 
 OP_DTYPE = np.dtype([("kind", "<u4"), ("q0", "<u4"), ("q1", "<u4"), ("_pad", "<u4"), ("theta", "<f8")])

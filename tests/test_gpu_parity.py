@@ -319,6 +319,20 @@ def test_c3_all_slots_c64(T, torch, oracle_runs):
     assert stats["draws"] == cfg.shots
 
 
+def test_c3_all_slots_no_live(T, torch, oracle_runs):
+    # the plain dense path (TUSQ_EXEC_NO_LIVE: every sweep visits the whole state, every sampled
+    # state stored) gives the same slots as the oracle -- and so as the default path
+    cfg = W.config("C3")
+    t = _tree(T, cfg)
+    slots, stats = T.run_tree(t, 128, flags=T.EXEC_NO_LIVE)
+    ref, edge = oracle_runs.sparse_run("C3")
+    _check_slots(slots, ref, edge, cfg.shots)
+    d = dstate(torch, cfg.n, 128)
+    T.run_tree(t, 128, d_state=d, leaf_begin=100, leaf_end=140, flags=T.EXEC_NO_LIVE | T.EXEC_NO_SAMPLE)
+    torch.cuda.synchronize()
+    assert float(np.abs(d.cpu().numpy() - oracle_runs.tree("C3").replay_leaf_core(139)).max()) <= 1e-10
+
+
 def test_c4_spot_leaves(T, torch, oracle_runs):
     # C4 (30 qubits, 16 GiB c128) in bench's launch configuration (fused, hybrid re-anchor):
     # SURVEY 8(d)'s 9 spot-check leaves (all-I, first 2, last 2, 4 seeded) plus the 2 leaves of

@@ -216,6 +216,10 @@ def test_live_tile_plan(lib):
     _, s = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY)
     full = 2.0 * (1 << cfg.n) * 16
     assert s["sweeps"] > 0 and s["hbm_bytes"] < 0.7 * s["sweeps"] * full
+    # the plain dense path (TUSQ_EXEC_NO_LIVE): same schedule, every sweep over the whole state
+    _, d = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY | lib.EXEC_NO_LIVE)
+    assert d["sweeps"] == s["sweeps"] and d["gate_apps"] == s["gate_apps"]
+    assert d["hbm_bytes"] >= 0.5 * d["sweeps"] * full > s["hbm_bytes"]
     # one H on a low qubit after a reset: the reset group is one tile, written as one tile
     n = 20
     ops = [W.op(W.X, 15), W.op(W.H, 3)]
