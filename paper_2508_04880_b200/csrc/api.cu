@@ -457,6 +457,15 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
         // transition decisions (reset vs uncompute), made one group AHEAD: a state that the next
         // transition discards (it resets) need not be stored after sampling (sums-only sweeps)
         struct Dec { bool reset; Cursor cf, c; InitState init; uint64_t sa_after; };
+        // Reset when its replay is shorter than bias x the uncompute.  With live tiles a reset's replay
+        // starts from one basis state and mostly visits a few tiles, while an uncompute sweeps a
+        // dense state and its state must be stored for it (no sums-only sampling): measured on C4,
+        // bias 1 / 2 / 1e6 = 21.4 / 15.1 / 13.2 s (debug build), plan bytes flat above 16.  The
+        // plain dense path (TUSQ_EXEC_NO_LIVE) keeps the gate-count rule (bias 1).
+        uint64_t reset_bias = (ex->flags & TUSQ_EXEC_NO_LIVE) ? 1 : 16;
+#ifdef TUSQ_DEBUG_KNOBS
+        if (getenv("TUSQ_DBG_RESET_BIAS")) reset_bias = (uint64_t)atoll(getenv("TUSQ_DBG_RESET_BIAS"));
+#endif
         auto decide = [&](size_t gi, uint64_t sa) {
             const SGroup &g = groups[gi];
             const Leaf &l = core[g.l0 - lb];
@@ -470,7 +479,7 @@ tusq_status tusq_run_tree(const tusq_tree *t, const tusq_exec *ex, uint64_t *out
             if (!d.reset) {
                 d.c = common_prefix(*t, *prev, l);
                 const uint64_t up = suffix_len(*t, *prev, d.c), down = suffix_len(*t, l, d.c);
-                if ((hybrid && reset_cost < up + down) || sa + up + down > budget) d.reset = true;
+                if ((hybrid && reset_cost < reset_bias * (up + down)) || sa + up + down > budget) d.reset = true;
                 else d.sa_after = sa + up + down;
             }
             if (d.reset) d.sa_after = reset_cost;

@@ -144,12 +144,13 @@ def test_partition_contiguous_and_balanced(lib):
 
 def test_sharded_plan_only(lib):
     # sharded mode's host logic (no device): same scheduler as replica mode (gate applications,
-    # leaves), global<->local exchanges only where a dense gate meets a global qubit
+    # leaves), global<->local exchanges only where a dense gate meets a global qubit.  Sharded mode
+    # has no live tiles, so it keeps the gate-count reset rule of the plain dense path (NO_LIVE)
     for name in ("C2a", "C2b", "C3"):
         cfg = W.config(name)
         nz = cfg.noise
         t = lib.build_error_tree(cfg.n, cfg.ops, nz.p1, nz.p2, nz.p_meas, cfg.shots, cfg.seed)
-        _, rep = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY)
+        _, rep = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY | lib.EXEC_NO_LIVE)
         for R in (2, 4, 8):
             _, s = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY, comm=lib.Comm.local(R))
             assert s["gate_apps"] == rep["gate_apps"] and s["leaves"] == rep["leaves"]
@@ -216,9 +217,10 @@ def test_live_tile_plan(lib):
     _, s = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY)
     full = 2.0 * (1 << cfg.n) * 16
     assert s["sweeps"] > 0 and s["hbm_bytes"] < 0.7 * s["sweeps"] * full
-    # the plain dense path (TUSQ_EXEC_NO_LIVE): same schedule, every sweep over the whole state
+    # the plain dense path (TUSQ_EXEC_NO_LIVE): every sweep over the whole state (and the gate-count
+    # reset rule, so a slightly different schedule: live tiles make resets cheaper than uncomputes)
     _, d = lib.run_tree(t, 128, flags=lib.EXEC_PLAN_ONLY | lib.EXEC_NO_LIVE)
-    assert d["sweeps"] == s["sweeps"] and d["gate_apps"] == s["gate_apps"]
+    assert d["leaves"] == s["leaves"] and d["resets"] <= s["resets"]
     assert d["hbm_bytes"] >= 0.5 * d["sweeps"] * full > s["hbm_bytes"]
     # one H on a low qubit after a reset: the reset group is one tile, written as one tile
     n = 20
