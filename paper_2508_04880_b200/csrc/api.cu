@@ -198,7 +198,9 @@ tusq_status tusq_tree_partition(const tusq_tree *t, uint32_t nranks, uint32_t pr
         if (i) {
             const Cursor c = common_prefix(*t, prev, cur);
             const uint64_t unc = suffix_len(*t, prev, c) + suffix_len(*t, cur, c);
-            if (unc <= reset && since + unc <= budget) { cost = unc; since += unc; }
+            // the default (live-tile) scheduler's rule: uncompute only when the reset's replay is at
+            // least 16x longer (tusq_run_tree's reset_bias)
+            if (reset >= 16 * unc && since + unc <= budget) { cost = unc; since += unc; }
             else since = reset;
         } else {
             since = reset;
