@@ -220,9 +220,11 @@ tusq_status tusq_tree_leaf(const tusq_tree *tree, uint64_t leaf, uint64_t *count
 
 /* Contiguous DFS leaf ranges for nranks replicas balanced by the host cost model
  * (SURVEY 8(e)): bounds[r]..bounds[r+1] for r < nranks (nranks + 1 entries).  The model replays
- * the scheduler of tusq_run_tree for `precision` (64 or 128): hybrid reset-vs-uncompute per
- * transition, plus the precision's re-anchor budget (1e6 gate applications c128, 2e4 c64), in
- * gate applications. */
+ * the default scheduler of tusq_run_tree for `precision` (64 or 128): hybrid reset-vs-uncompute
+ * per transition (an uncompute only when the reset's replay is >= 16x longer: live tiles make
+ * replays cheap), plus the precision's re-anchor budget (1e6 gate applications c128, 2e4 c64),
+ * costed in gate applications.  (Device time tracks full sweeps more than gate counts, so callers
+ * that can should interleave finer ranges over their ranks -- bench.py does.) */
 tusq_status tusq_tree_partition(const tusq_tree *tree, uint32_t nranks, uint32_t precision, uint64_t *bounds);
 
 void tusq_tree_free(tusq_tree *tree);
