@@ -11,7 +11,7 @@ for w in $WHAT; do
     bench) timeout 1800 python bench.py $BARGS > $O/bench.log 2>&1; echo "bench rc=$?" >> $O/rc.txt ;;
     kb) timeout 900 python scripts/kernel_bench.py > $O/kb.json 2> $O/kb.err; echo "kb rc=$?" >> $O/rc.txt ;;
     ncu) timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches.csv python bench.py --steps 40 --warmup 0 --no-cpu-baseline --profile-leaves 4 > $O/ncu_bench.log 2>&1; echo "ncu-list rc=$?" >> $O/rc.txt
-         timeout 1800 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 40 -c 4 -o $O/k_fused_full python bench.py --steps 40 --warmup 0 --no-cpu-baseline --profile-leaves 4 > $O/ncu_full.log 2>&1; echo "ncu-full rc=$?" >> $O/rc.txt ;;
+         timeout 1800 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 40 -c 1 -o $O/k_fused_full python bench.py --steps 40 --warmup 0 --no-cpu-baseline --profile-leaves 4 > $O/ncu_full.log 2>&1; echo "ncu-full rc=$?" >> $O/rc.txt ;;
   esac
 done
 tail -5 $O/pytest.log 2>/dev/null; cat $O/rc.txt; tail -c 3000 $O/bench.log 2>/dev/null
