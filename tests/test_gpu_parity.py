@@ -308,6 +308,25 @@ def test_c3_all_slots(T, torch, oracle_runs):
     assert stats["draws"] == cfg.shots
 
 
+def test_c3_continued_batches(T, torch, oracle_runs):
+    # bench.py's launch configuration at N = 1: the range split into contiguous batches, each call
+    # continuing the DFS state the previous one left (TUSQ_EXEC_CONTINUE) -- the valid-set /
+    # sums-only bookkeeping must hand over a whole, stored state at every call boundary
+    cfg = W.config("C3")
+    t = _tree(T, cfg)
+    b = t.partition(5)
+    d = dstate(torch, cfg.n, 128)
+    slots = np.zeros(cfg.shots, dtype=np.uint64)
+    for s_ in range(5):
+        T.run_tree(t, 128, d_state=d, leaf_begin=int(b[s_]), leaf_end=int(b[s_ + 1]),
+                   flags=T.EXEC_CONTINUE if s_ else 0, out_slots=slots)
+    ref, edge = oracle_runs.sparse_run("C3")
+    _check_slots(slots, ref, edge, cfg.shots)
+    torch.cuda.synchronize()
+    last = t.n_leaves - 1
+    assert float(np.abs(d.cpu().numpy() - oracle_runs.tree("C3").replay_leaf_core(last)).max()) <= 1e-10
+
+
 def test_c3_all_slots_c64(T, torch, oracle_runs):
     # the same at complex64 (fp64 CDF sums; edge window 1e-5, reading #17): exercises the c64 K5
     # path with live tiles, valid sets and sums-only sampling (replayed tiles) at 24 qubits
